@@ -1,0 +1,418 @@
+"""B200-native tensor transposition engine (arXiv:1603.02297, Eq. 1).
+
+    B_perm(i1..iN) <- alpha * A(i1..iN) + beta * B_perm(i1..iN)
+
+Python mirror of the reference's interface (ttune, /root/reference/proj):
+``make_problem``/``validate``/``merge_indices``/``canonical_key`` of
+problem.hpp, ``TensorBuffer``/``make_buffer_a``/``make_buffer_b``/
+``reference_transpose``/``execute_plan`` of executor.hpp and ``bandwidth`` of
+tuner.hpp -- same names, argument meaning and error behaviour
+(``std::invalid_argument`` -> ``ValueError`` with the same text).  Every call
+goes through the C ABI of libttb.so (include/ttb.h); buffers live in device
+memory (torch CUDA tensors are used only as HBM allocations) and the work is
+done by the sm_100a kernels.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+from . import _lib
+from ._lib import TTBError, check, ints, last_error, lib, longs
+
+__all__ = [
+    "ElementKind", "Permutation", "TransposeProblem", "NormalizedProblem", "MergeRecord",
+    "make_problem", "validate", "sizes_b", "element_strides_a", "element_strides_b",
+    "element_strides_b_for_a", "b_stride1_axis", "required_elements_a", "required_elements_b",
+    "canonical_key", "merge_indices", "TensorBuffer", "make_buffer_a", "make_buffer_b",
+    "reference_transpose", "execute_plan", "GpuPlan", "bandwidth_gbs", "shard_boxes",
+    "fill_uniform", "fill_sentinel", "checksum", "launch_count", "TTBError", "version",
+]
+
+
+class ElementKind(enum.IntEnum):
+    """problem.hpp:11 -- codes s/d/c/z."""
+    real32 = 0
+    real64 = 1
+    complex64 = 2
+    complex128 = 3
+
+    @property
+    def code(self) -> str:
+        return "sdcz"[self]
+
+    @property
+    def bytes(self) -> int:
+        return (4, 8, 8, 16)[self]
+
+    @property
+    def components(self) -> int:
+        return 2 if self >= 2 else 1
+
+    @classmethod
+    def from_code(cls, c: str) -> "ElementKind":
+        return cls("sdcz".index(c))
+
+
+def _kind(k) -> ElementKind:
+    if isinstance(k, str):
+        return ElementKind.from_code(k)
+    return ElementKind(int(k))
+
+
+@dataclass
+class Permutation:
+    """1-based scatter map: map[a] is B's position of A index a+1 (problem.hpp:22-35)."""
+    map: List[int]
+
+    def rank(self) -> int:
+        return len(self.map)
+
+    def is_valid(self) -> bool:
+        n = len(self.map)
+        return n > 0 and sorted(self.map) == list(range(1, n + 1))
+
+    def is_identity(self) -> bool:
+        return self.rank() > 0 and all(v == a + 1 for a, v in enumerate(self.map))
+
+    def preserves_stride1(self) -> bool:
+        return bool(self.map) and self.map[0] == 1
+
+    def inverse(self) -> "Permutation":
+        inv = [0] * len(self.map)
+        for a, v in enumerate(self.map):
+            inv[v - 1] = a + 1
+        return Permutation(inv)
+
+    @classmethod
+    def from_gather(cls, gather: Sequence[int]) -> "Permutation":
+        """Paper/BASELINE tuple (B index k is A index gather[k], 0-based)."""
+        m = [0] * len(gather)
+        for k, a in enumerate(gather):
+            m[a] = k + 1
+        return cls(m)
+
+
+@dataclass
+class TransposeProblem:
+    """problem.hpp:37-49."""
+    perm: Permutation
+    sizes: List[int]
+    lda: List[int]
+    ldb: List[int]
+    alpha: float = 1.0
+    beta: float = 0.0
+    kind_a: ElementKind = ElementKind.real32
+    kind_b: ElementKind = ElementKind.real32
+
+    def rank(self) -> int:
+        return self.perm.rank()
+
+    def total_elements(self) -> int:
+        n = 1
+        for s in self.sizes:
+            n *= s
+        return n
+
+    def _args(self):
+        n = self.rank()
+        return (int(self.kind_a), int(self.kind_b), n, ints(self.perm.map), longs(self.sizes),
+                longs(self.lda), longs(self.ldb))
+
+
+def make_problem(perm_map: Sequence[int], sizes: Sequence[int], kind_a=ElementKind.real32,
+                 kind_b=ElementKind.real32, alpha: float = 1.0, beta: float = 0.0,
+                 lda: Optional[Sequence[int]] = None,
+                 ldb: Optional[Sequence[int]] = None) -> TransposeProblem:
+    """problem.hpp:51-58: lda defaults to sizes, ldb to sizes_b (dense)."""
+    p = TransposeProblem(Permutation(list(perm_map)), list(sizes), [], [], float(alpha),
+                         float(beta), _kind(kind_a), _kind(kind_b))
+    p.lda = list(lda) if lda else list(p.sizes)
+    if ldb:
+        p.ldb = list(ldb)
+    elif p.perm.is_valid() and len(p.sizes) == p.rank():
+        p.ldb = sizes_b(p)
+    return p
+
+
+def validate(p: TransposeProblem) -> TransposeProblem:
+    """problem.cpp:107-159, checked natively; raises ValueError with the reference's text."""
+    check(lib.ttb_validate(len(p.perm.map), ints(p.perm.map), len(p.sizes), longs(p.sizes),
+                           len(p.lda), longs(p.lda), len(p.ldb), longs(p.ldb), int(p.kind_a),
+                           int(p.kind_b)))
+    return p
+
+
+def sizes_b(p: TransposeProblem) -> List[int]:
+    sb = [0] * p.rank()
+    for a, k in enumerate(p.perm.map):
+        sb[k - 1] = p.sizes[a]
+    return sb
+
+
+def _prefix(ld):
+    out, acc = [], 1
+    for v in ld:
+        out.append(acc)
+        acc *= v
+    return out
+
+
+def element_strides_a(p: TransposeProblem) -> List[int]:
+    return _prefix(p.lda)
+
+
+def element_strides_b(p: TransposeProblem) -> List[int]:
+    return _prefix(p.ldb)
+
+
+def element_strides_b_for_a(p: TransposeProblem) -> List[int]:
+    sb = element_strides_b(p)
+    return [sb[k - 1] for k in p.perm.map]
+
+
+def b_stride1_axis(p: TransposeProblem) -> int:
+    return p.perm.map.index(1) if 1 in p.perm.map else -1
+
+
+def required_elements_a(p: TransposeProblem) -> int:
+    return lib.ttb_required_elements_a(p.rank(), longs(p.sizes), longs(p.lda))
+
+
+def required_elements_b(p: TransposeProblem) -> int:
+    return lib.ttb_required_elements_b(p.rank(), ints(p.perm.map), longs(p.sizes), longs(p.ldb))
+
+
+def canonical_key(p: TransposeProblem) -> str:
+    buf = C.create_string_buffer(4096)
+    check(lib.ttb_canonical_key(*p._args(), p.alpha, p.beta, buf, 4096))
+    return buf.value.decode()
+
+
+@dataclass
+class MergeRecord:
+    from_first: int
+    from_last: int
+    to: int
+
+
+@dataclass
+class NormalizedProblem:
+    problem: TransposeProblem
+    merge_trace: List[MergeRecord] = field(default_factory=list)
+
+
+def merge_indices(p: TransposeProblem) -> NormalizedProblem:
+    """problem.cpp:270-340 (native)."""
+    validate(p)
+    n = p.rank()
+    r = C.c_int(0)
+    op, os_ = (C.c_int * n)(), (C.c_int64 * n)()
+    ola, olb = (C.c_int64 * n)(), (C.c_int64 * n)()
+    lo, hi = (C.c_int * n)(), (C.c_int * n)()
+    check(lib.ttb_merge_indices(n, ints(p.perm.map), longs(p.sizes), longs(p.lda), longs(p.ldb),
+                                C.byref(r), op, os_, ola, olb, lo, hi))
+    k = r.value
+    q = TransposeProblem(Permutation(list(op[:k])), list(os_[:k]), list(ola[:k]), list(olb[:k]),
+                         p.alpha, p.beta, p.kind_a, p.kind_b)
+    return NormalizedProblem(q, [MergeRecord(lo[i], hi[i], i + 1) for i in range(k)])
+
+
+def bandwidth_gbs(p: TransposeProblem, seconds: float) -> float:
+    """tuner.cpp:18-25 byte count, decimal GB/s."""
+    v = lib.ttb_bandwidth_gbs(int(p.kind_a), int(p.kind_b), p.total_elements(), p.beta, seconds)
+    if v < 0:
+        raise ValueError("bandwidth: time must be positive")
+    return v
+
+
+def debug_candidates(p: TransposeProblem) -> List[str]:
+    """The planner's ranked candidates for p (host only, no device needed)."""
+    buf = C.create_string_buffer(1 << 14)
+    check(lib.ttb_debug_candidates(*p._args(), p.alpha, p.beta, buf, 1 << 14))
+    return [s for s in buf.value.decode().split("\n") if s]
+
+
+def version() -> str:
+    return lib.ttb_version().decode()
+
+
+def launch_count() -> int:
+    return int(lib.ttb_launch_count())
+
+
+# ----------------------------------------------------------------- buffers --
+
+def _torch():
+    import torch  # noqa: PLC0415  (device memory only)
+    return torch
+
+
+class TensorBuffer:
+    """Element-kind tagged DEVICE storage (executor.hpp:45-70).  Backed by a
+    torch CUDA tensor of scalars (complex kinds: interleaved re/im)."""
+
+    def __init__(self, kind, elements: int, device=None, tensor=None):
+        torch = _torch()
+        self._kind = _kind(kind)
+        if elements < 0:
+            raise ValueError("buffer: negative element count")
+        self._elements = int(elements)
+        dt = torch.float64 if self._kind in (ElementKind.real64, ElementKind.complex128) \
+            else torch.float32
+        n = self._elements * self._kind.components
+        if tensor is None:
+            tensor = torch.zeros(n, dtype=dt, device=device or "cuda")
+        elif tensor.numel() < n or tensor.dtype != dt or not tensor.is_cuda:
+            raise ValueError("buffer: tensor does not match kind/elements on a CUDA device")
+        self.tensor = tensor
+
+    def kind(self) -> ElementKind:
+        return self._kind
+
+    def elements(self) -> int:
+        return self._elements
+
+    def scalars(self) -> int:
+        return self._elements * self._kind.components
+
+    def bytes(self) -> int:
+        return self._elements * self._kind.bytes
+
+    def data_ptr(self) -> int:
+        return self.tensor.data_ptr()
+
+
+def make_buffer_a(p: TransposeProblem, device=None) -> TensorBuffer:
+    return TensorBuffer(p.kind_a, required_elements_a(validate(p)), device)
+
+
+def make_buffer_b(p: TransposeProblem, device=None) -> TensorBuffer:
+    return TensorBuffer(p.kind_b, required_elements_b(validate(p)), device)
+
+
+def _stream(stream):
+    if stream is None:
+        return C.c_void_p(_torch().cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return C.c_void_p(stream)
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _check_kinds(p: TransposeProblem, a: TensorBuffer, b: TensorBuffer):
+    if a.kind() != p.kind_a:
+        raise ValueError("A buffer: element kind mismatch")
+    if b.kind() != p.kind_b:
+        raise ValueError("B buffer: element kind mismatch")
+
+
+def reference_transpose(p: TransposeProblem, a: TensorBuffer, b: TensorBuffer,
+                        stream=None) -> None:
+    """executor.hpp:80-83 on the GPU: plan from the cache (heuristic on a miss),
+    asynchronous on `stream` (default: torch's current stream)."""
+    validate(p)
+    _check_kinds(p, a, b)
+    check(lib.ttb_transpose(*p._args(), p.alpha, C.c_void_p(a.data_ptr()), a.elements(), p.beta,
+                            C.c_void_p(b.data_ptr()), b.elements(), _stream(stream)))
+
+
+class GpuPlan:
+    """The sm_100a counterpart of ttune::CandidatePlan (plan.hpp) plus its
+    executor: variant, tile, vector widths, launch shape for one problem."""
+
+    def __init__(self, p: TransposeProblem, cache: bool = True):
+        validate(p)
+        self.problem = p
+        h = C.c_void_p()
+        check(lib.ttb_plan_create(C.byref(h), *p._args(), p.alpha, p.beta, 0 if cache else 1))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.ttb_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
+
+    def execute(self, a, b, stream=None) -> None:
+        pa = a.data_ptr() if hasattr(a, "data_ptr") else int(a)
+        pb = b.data_ptr() if hasattr(b, "data_ptr") else int(b)
+        check(lib.ttb_plan_execute(self._h, C.c_void_p(pa), C.c_void_p(pb), _stream(stream)))
+
+    def execute_host(self, a_host, b_host) -> None:
+        """End-to-end on host (numpy/pinned torch) buffers: H2D, kernel, D2H."""
+        pa = a_host.ctypes.data if hasattr(a_host, "ctypes") else a_host.data_ptr()
+        pb = b_host.ctypes.data if hasattr(b_host, "ctypes") else b_host.data_ptr()
+        check(lib.ttb_plan_execute_host(self._h, C.c_void_p(pa), C.c_void_p(pb)))
+
+    def autotune(self, a, b, warmups: int = 2, reps: int = 3, stream=None) -> str:
+        pa = a.data_ptr() if hasattr(a, "data_ptr") else int(a)
+        pb = b.data_ptr() if hasattr(b, "data_ptr") else int(b)
+        check(lib.ttb_plan_autotune(self._h, C.c_void_p(pa), C.c_void_p(pb), warmups, reps,
+                                    _stream(stream)))
+        return self.describe()
+
+    def describe(self) -> str:
+        buf = C.create_string_buffer(512)
+        check(lib.ttb_plan_describe(self._h, buf, 512))
+        return buf.value.decode()
+
+    def candidates(self) -> List[str]:
+        buf = C.create_string_buffer(1 << 14)
+        check(lib.ttb_plan_candidates(self._h, buf, 1 << 14))
+        return [s for s in buf.value.decode().split("\n") if s]
+
+    def select(self, text: str) -> None:
+        check(lib.ttb_plan_select(self._h, text.encode()))
+
+
+def execute_plan(p: TransposeProblem, plan: Optional[GpuPlan], a: TensorBuffer, b: TensorBuffer,
+                 stream=None) -> None:
+    """executor.hpp:85-88: run a given plan (None = cached heuristic plan)."""
+    if plan is None:
+        return reference_transpose(p, a, b, stream)
+    validate(p)
+    _check_kinds(p, a, b)
+    if a.elements() < required_elements_a(p):
+        raise ValueError("A buffer: too small for problem")
+    if b.elements() < required_elements_b(p):
+        raise ValueError("B buffer: too small for problem")
+    plan.execute(a, b, stream)
+
+
+# --------------------------------------------------------- partition/data --
+
+def shard_boxes(p: TransposeProblem, world: int, rank: int) -> List[Tuple[List[int], List[int]]]:
+    """Boxes (origin, extent in A order) of `rank`'s slab of B."""
+    n = p.rank()
+    cnt = C.c_int(0)
+    check(lib.ttb_shard_boxes(n, ints(p.perm.map), longs(p.sizes), world, rank, None, None,
+                              C.byref(cnt)))
+    o, e = (C.c_int64 * (cnt.value * n))(), (C.c_int64 * (cnt.value * n))()
+    check(lib.ttb_shard_boxes(n, ints(p.perm.map), longs(p.sizes), world, rank, o, e,
+                              C.byref(cnt)))
+    return [(list(o[i * n:(i + 1) * n]), list(e[i * n:(i + 1) * n])) for i in range(cnt.value)]
+
+
+def fill_uniform(kind, sizes, ld, seed: int, ptr: int, origin=None, global_sizes=None,
+                 stream=None) -> None:
+    check(lib.ttb_fill_uniform(int(_kind(kind)), len(sizes), longs(sizes), longs(ld),
+                               longs(origin), longs(global_sizes), seed, C.c_void_p(ptr),
+                               _stream(stream)))
+
+
+def fill_sentinel(kind, elements: int, ptr: int, stream=None) -> None:
+    check(lib.ttb_fill_sentinel(int(_kind(kind)), elements, C.c_void_p(ptr), _stream(stream)))
+
+
+def checksum(kind, sizes, ld, ptr: int, origin=None, global_sizes=None, stream=None) -> int:
+    out = C.c_uint64(0)
+    check(lib.ttb_checksum(int(_kind(kind)), len(sizes), longs(sizes), longs(ld), longs(origin),
+                           longs(global_sizes), C.c_void_p(ptr), C.byref(out), _stream(stream)))
+    return out.value

@@ -1,0 +1,532 @@
+// api.cpp -- the extern "C" boundary (include/ttb.h).
+//
+// Mirrors the reference's entry points (executor.hpp:80-88, problem.hpp:51-102,
+// tuner.hpp:53-62): problem checks with the reference's messages, an
+// in-memory plan cache keyed by canonical_key (problem.cpp:228-241) plus the
+// device, CUDA-event autotuning, and the stream-ordered launch.  No exception
+// crosses the ABI; failures become status codes plus ttb_last_error().
+#include "../../include/ttb.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "launch.hpp"
+#include "plan.hpp"
+#include "problem.hpp"
+
+namespace ttb {
+unsigned long long launch_total();
+}
+
+using namespace ttb;
+
+namespace {
+
+thread_local std::string t_err;
+
+int ok() {
+  t_err.clear();
+  return TTB_OK;
+}
+
+int fail(int code, const std::string& msg) {
+  t_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(e == cudaErrorMemoryAllocation ? TTB_ENOMEM : TTB_ECUDA,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+std::vector<int64_t> vec64(const int64_t* p, int n) {
+  return p ? std::vector<int64_t>(p, p + n) : std::vector<int64_t>{};
+}
+
+Problem from_args(int ka, int kb, int rank, const int* perm, const int64_t* sizes,
+                  const int64_t* lda, const int64_t* ldb, double alpha, double beta) {
+  std::vector<int> pm = perm && rank > 0 ? std::vector<int>(perm, perm + rank) : std::vector<int>{};
+  return make(std::move(pm), vec64(sizes, std::max(rank, 0)), ka, kb, alpha, beta,
+              vec64(lda, std::max(rank, 0)), vec64(ldb, std::max(rank, 0)));
+}
+
+int current_device(int* dev, int* sms) {
+  cudaError_t e = cudaGetDevice(dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  e = cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, *dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  return TTB_OK;
+}
+
+}  // namespace
+
+struct ttb_plan_s {
+  Problem orig;
+  Merged merged;
+  Geo geo;
+  std::vector<Spec> cands;
+  Prepared prep;      // chosen variant
+  Prepared fallback;  // element-aligned variant for misaligned buffers
+  int device = 0, sms = 148;
+  std::string key;    // canonical_key + device
+  bool cached = true;
+  // end-to-end staging (ttb_plan_execute_host)
+  void* dA = nullptr;
+  void* dB = nullptr;
+  cudaStream_t hs = nullptr;
+  ~ttb_plan_s() {
+    if (dA) cudaFree(dA);
+    if (dB) cudaFree(dB);
+    if (hs) cudaStreamDestroy(hs);
+  }
+  size_t bytes_a() const { return static_cast<size_t>(orig.footprint_a()) * kind_bytes(orig.kind_a); }
+  size_t bytes_b() const { return static_cast<size_t>(orig.footprint_b()) * kind_bytes(orig.kind_b); }
+};
+
+namespace {
+
+std::mutex g_mu;
+std::unordered_map<std::string, std::string> g_choice;                 // key -> spec text
+std::unordered_map<std::string, std::unique_ptr<ttb_plan_s>> g_plans;  // one-shot API plans
+
+int build_plan(const Problem& p, int flags, std::unique_ptr<ttb_plan_s>* out) {
+  auto pl = std::make_unique<ttb_plan_s>();
+  pl->orig = p;
+  pl->merged = fuse_indices(p);
+  if (pl->merged.p.rank() > kMaxRank)
+    return fail(TTB_EINVAL, "perm: rank " + std::to_string(pl->merged.p.rank()) +
+                                " after merging exceeds TTB_MAX_RANK");
+  pl->geo = make_geo(pl->merged.p);
+  pl->cands = candidates(pl->geo);
+  int rc = current_device(&pl->device, &pl->sms);
+  if (rc) return rc;
+  pl->key = cache_key(p) + "@dev" + std::to_string(pl->device);
+  pl->cached = !(flags & TTB_PLAN_NO_CACHE);
+  std::string why;
+  bool have = false;
+  if (pl->cached) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_choice.find(pl->key);
+    Spec s;
+    if (it != g_choice.end() && Spec::parse(it->second, &s))
+      have = prepare(pl->geo, s, pl->sms, &pl->prep, &why);
+  }
+  for (size_t i = 0; !have && i < pl->cands.size(); ++i)
+    have = prepare(pl->geo, pl->cands[i], pl->sms, &pl->prep, &why);
+  if (!have) return fail(TTB_EINTERNAL, "plan: no applicable kernel variant (" + why + ")");
+  if (!prepare(pl->geo, pl->cands.back(), pl->sms, &pl->fallback, &why)) pl->fallback = pl->prep;
+  cudaError_t e = cudaGetLastError();  // occupancy queries surface context errors here
+  if (e != cudaSuccess) return cuda_fail(e, "plan");
+  *out = std::move(pl);
+  return TTB_OK;
+}
+
+cudaError_t launch(const Geo& g, Prepared pr, const void* A, void* B, cudaStream_t s) {
+  switch (pr.spec.v) {
+    case kCopy:
+      pr.cp.A = A;
+      pr.cp.B = B;
+      return launch_copy(g.ka, g.kb, pr.spec.w1, pr.mode, pr.cp, pr.l, s);
+    case kRt:
+      pr.rp.A = A;
+      pr.rp.B = B;
+      return launch_rt(g.ka, g.kb, pr.spec.w1, pr.spec.w2, pr.mode, pr.rp, pr.l, s);
+    default:
+      pr.sp.A = A;
+      pr.sp.B = B;
+      return launch_smem(g.ka, g.kb, pr.mode, pr.sp, pr.l, s);
+  }
+}
+
+bool aligned(const void* p, int a) { return reinterpret_cast<uintptr_t>(p) % static_cast<uintptr_t>(a) == 0; }
+
+// alpha/beta come from the call: one-shot plans are shared by every problem
+// with the same canonical key and update mode (move / scale / update)
+int execute(ttb_plan_s* pl, const Prepared& pr0, const void* A, void* B, cudaStream_t s,
+            double alpha, double beta) {
+  if (!A) return fail(TTB_EINVAL, "A buffer: null pointer");
+  if (!B) return fail(TTB_EINVAL, "B buffer: null pointer");
+  const Prepared* pr = &pr0;
+  if (!aligned(A, pr->a_align) || !aligned(B, pr->b_align)) pr = &pl->fallback;
+  if (!aligned(A, pr->a_align)) return fail(TTB_EINVAL, "A buffer: misaligned for its element kind");
+  if (!aligned(B, pr->b_align)) return fail(TTB_EINVAL, "B buffer: misaligned for its element kind");
+  Prepared run = *pr;
+  run.cp.sc = run.rp.sc = run.sp.sc = Scale{alpha, beta};
+  const cudaError_t e = launch(pl->geo, run, A, B, s);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return ok();
+}
+
+template <class Fn>
+int guarded(Fn&& fn) {
+  try {
+    return fn();
+  } catch (const InvalidArgument& e) {
+    return fail(TTB_EINVAL, e.what);
+  } catch (const std::bad_alloc&) {
+    return fail(TTB_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(TTB_EINTERNAL, e.what());
+  } catch (...) {
+    return fail(TTB_EINTERNAL, "unknown error");
+  }
+}
+
+int box_params(int kind, int rank, const int64_t* sizes, const int64_t* ld, const int64_t* origin,
+               const int64_t* gsizes, BoxParams* bp) {
+  if (rank < 1 || rank > 16 || !sizes) return fail(TTB_EINVAL, "box: bad rank");
+  if (kind < 0 || kind > 3) return fail(TTB_EINVAL, "box: bad kind");
+  bp->rank = rank;
+  bp->C = kind_components(kind);
+  int64_t acc = 1, gacc = 1;
+  bp->gbase = 0;
+  bp->total = 1;
+  for (int d = 0; d < rank; ++d) {
+    if (sizes[d] < 1) return fail(TTB_EINVAL, "box: extent < 1");
+    bp->ext[d] = sizes[d];
+    bp->st[d] = acc;
+    acc *= ld ? ld[d] : sizes[d];
+    bp->gst[d] = gacc;
+    if (origin) bp->gbase += origin[d] * gacc;
+    gacc *= gsizes ? gsizes[d] : sizes[d];
+    bp->total *= sizes[d];
+  }
+  return TTB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ttb_last_error(void) { return t_err.c_str(); }
+const char* ttb_version(void) { return TTB_VERSION; }
+
+int ttb_validate(int n_perm, const int* perm, int n_sizes, const int64_t* sizes, int n_lda,
+                 const int64_t* lda, int n_ldb, const int64_t* ldb, int kind_a, int kind_b) {
+  return guarded([&] {
+    Problem p = make(perm ? std::vector<int>(perm, perm + std::max(n_perm, 0)) : std::vector<int>{},
+                     vec64(sizes, std::max(n_sizes, 0)), kind_a, kind_b, 1.0, 0.0,
+                     n_lda >= 0 ? vec64(lda, n_lda) : std::vector<int64_t>{},
+                     n_ldb >= 0 ? vec64(ldb, n_ldb) : std::vector<int64_t>{});
+    // an explicitly empty lda/ldb (n = 0) must still be reported as such
+    if (n_lda == 0) p.lda.clear();
+    if (n_ldb == 0) p.ldb.clear();
+    check(p);
+    return ok();
+  });
+}
+
+int64_t ttb_required_elements_a(int rank, const int64_t* sizes, const int64_t* lda) {
+  if (rank < 1 || !sizes) return -1;
+  Problem p;
+  p.sizes = vec64(sizes, rank);
+  p.lda = lda ? vec64(lda, rank) : p.sizes;
+  return p.footprint_a();
+}
+
+int64_t ttb_required_elements_b(int rank, const int* perm, const int64_t* sizes,
+                                const int64_t* ldb) {
+  if (rank < 1 || !sizes || !perm) return -1;
+  Problem p = make(std::vector<int>(perm, perm + rank), vec64(sizes, rank), 0, 0, 1.0, 0.0, {},
+                   ldb ? vec64(ldb, rank) : std::vector<int64_t>{});
+  if (p.ldb.size() != static_cast<size_t>(rank)) return -1;
+  return p.footprint_b();
+}
+
+int ttb_merge_indices(int rank, const int* perm, const int64_t* sizes, const int64_t* lda,
+                      const int64_t* ldb, int* out_rank, int* out_perm, int64_t* out_sizes,
+                      int64_t* out_lda, int64_t* out_ldb, int* trace_lo, int* trace_hi) {
+  return guarded([&] {
+    const Merged m = fuse_indices(from_args(0, 0, rank, perm, sizes, lda, ldb, 1.0, 0.0));
+    const int r = m.p.rank();
+    if (out_rank) *out_rank = r;
+    for (int a = 0; a < r; ++a) {
+      if (out_perm) out_perm[a] = m.p.perm[a];
+      if (out_sizes) out_sizes[a] = m.p.sizes[a];
+      if (out_lda) out_lda[a] = m.p.lda[a];
+      if (out_ldb) out_ldb[a] = m.p.ldb[a];
+      if (trace_lo) trace_lo[a] = m.runs[a].first;
+      if (trace_hi) trace_hi[a] = m.runs[a].second;
+    }
+    return ok();
+  });
+}
+
+int ttb_canonical_key(int kind_a, int kind_b, int rank, const int* perm, const int64_t* sizes,
+                      const int64_t* lda, const int64_t* ldb, double alpha, double beta,
+                      char* buf, size_t len) {
+  return guarded([&] {
+    const std::string k =
+        cache_key(from_args(kind_a, kind_b, rank, perm, sizes, lda, ldb, alpha, beta));
+    if (!buf || len <= k.size()) return fail(TTB_EINVAL, "canonical_key: buffer too small");
+    std::memcpy(buf, k.c_str(), k.size() + 1);
+    return ok();
+  });
+}
+
+double ttb_bandwidth_gbs(int kind_a, int kind_b, int64_t elements, double beta, double seconds) {
+  if (!(seconds > 0.0) || kind_a < 0 || kind_a > 3 || kind_b < 0 || kind_b > 3) return -1.0;
+  const double n = static_cast<double>(elements);
+  double bytes = n * kind_bytes(kind_a) + n * kind_bytes(kind_b);
+  if (beta != 0.0) bytes += n * kind_bytes(kind_b);
+  return bytes / 1e9 / seconds;
+}
+
+int ttb_plan_create(ttb_plan* out, int kind_a, int kind_b, int rank, const int* perm,
+                    const int64_t* sizes, const int64_t* lda, const int64_t* ldb, double alpha,
+                    double beta, int flags) {
+  return guarded([&] {
+    if (!out) return fail(TTB_EINVAL, "plan: null output handle");
+    *out = nullptr;
+    const Problem p = from_args(kind_a, kind_b, rank, perm, sizes, lda, ldb, alpha, beta);
+    check(p);
+    std::unique_ptr<ttb_plan_s> pl;
+    const int rc = build_plan(p, flags, &pl);
+    if (rc) return rc;
+    *out = pl.release();
+    return ok();
+  });
+}
+
+int ttb_plan_destroy(ttb_plan plan) {
+  delete plan;
+  return ok();
+}
+
+int ttb_plan_execute(ttb_plan plan, const void* A, void* B, ttb_stream stream) {
+  if (!plan) return fail(TTB_EINVAL, "plan: null handle");
+  return guarded([&] {
+    return execute(plan, plan->prep, A, B, reinterpret_cast<cudaStream_t>(stream), plan->orig.alpha,
+                   plan->orig.beta);
+  });
+}
+
+int ttb_transpose(int kind_a, int kind_b, int rank, const int* perm, const int64_t* sizes,
+                  const int64_t* lda, const int64_t* ldb, double alpha, const void* A,
+                  int64_t a_elements, double beta, void* B, int64_t b_elements,
+                  ttb_stream stream) {
+  return guarded([&] {
+    const Problem p = from_args(kind_a, kind_b, rank, perm, sizes, lda, ldb, alpha, beta);
+    check(p);  // validate first, then buffers (executor.cpp:373-374, 315-322)
+    if (a_elements >= 0 && a_elements < p.footprint_a())
+      return fail(TTB_EINVAL, "A buffer: too small for problem");
+    if (b_elements >= 0 && b_elements < p.footprint_b())
+      return fail(TTB_EINVAL, "B buffer: too small for problem");
+    int dev = 0, sms = 0;
+    int rc = current_device(&dev, &sms);
+    if (rc) return rc;
+    const int mode = p.beta != 0.0 ? 2 : (p.alpha == 1.0 ? 0 : 1);
+    const std::string key = cache_key(p) + "@dev" + std::to_string(dev) + "|m" + std::to_string(mode);
+    ttb_plan_s* pl = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      auto it = g_plans.find(key);
+      if (it != g_plans.end()) pl = it->second.get();
+    }
+    if (!pl) {
+      std::unique_ptr<ttb_plan_s> fresh;
+      rc = build_plan(p, TTB_PLAN_DEFAULT, &fresh);
+      if (rc) return rc;
+      std::lock_guard<std::mutex> lk(g_mu);
+      auto& slot = g_plans[key];
+      if (!slot) slot = std::move(fresh);
+      pl = slot.get();
+    }
+    return execute(pl, pl->prep, A, B, reinterpret_cast<cudaStream_t>(stream), alpha, beta);
+  });
+}
+
+int ttb_plan_execute_host(ttb_plan plan, const void* A_host, void* B_host) {
+  if (!plan) return fail(TTB_EINVAL, "plan: null handle");
+  return guarded([&] {
+    if (!A_host || !B_host) return fail(TTB_EINVAL, "host buffers: null pointer");
+    cudaError_t e;
+    const size_t na = plan->bytes_a(), nb = plan->bytes_b();
+    if (!plan->dA) {
+      if ((e = cudaMalloc(&plan->dA, na)) != cudaSuccess) return cuda_fail(e, "cudaMalloc A");
+      if ((e = cudaMalloc(&plan->dB, nb)) != cudaSuccess) return cuda_fail(e, "cudaMalloc B");
+      if ((e = cudaStreamCreateWithFlags(&plan->hs, cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_fail(e, "cudaStreamCreate");
+    }
+    cudaStream_t s = plan->hs;
+    // B's padding must come back unchanged, so B travels to the device when
+    // it is read (beta != 0) or padded
+    const bool b_in = plan->orig.beta != 0.0 ||
+                      plan->orig.footprint_b() != plan->orig.elements();
+    if ((e = cudaMemcpyAsync(plan->dA, A_host, na, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return cuda_fail(e, "H2D A");
+    if (b_in && (e = cudaMemcpyAsync(plan->dB, B_host, nb, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return cuda_fail(e, "H2D B");
+    const int rc = execute(plan, plan->prep, plan->dA, plan->dB, s, plan->orig.alpha, plan->orig.beta);
+    if (rc) return rc;
+    if ((e = cudaMemcpyAsync(B_host, plan->dB, nb, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return cuda_fail(e, "D2H B");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "sync");
+    return ok();
+  });
+}
+
+int ttb_plan_autotune(ttb_plan plan, const void* A, void* B, int warmups, int reps,
+                      ttb_stream stream) {
+  if (!plan) return fail(TTB_EINVAL, "plan: null handle");
+  return guarded([&] {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (warmups < 0 || reps < 1)
+      return fail(TTB_EINVAL, "protocol: need warmups >= 0 and repetitions >= 1");
+    void* target = B;
+    void* scratch = nullptr;
+    cudaError_t e;
+    if (plan->orig.beta != 0.0) {  // candidates must not keep updating the caller's B
+      if ((e = cudaMalloc(&scratch, plan->bytes_b())) != cudaSuccess) return cuda_fail(e, "scratch");
+      if ((e = cudaMemcpyAsync(scratch, B, plan->bytes_b(), cudaMemcpyDeviceToDevice, s)) != cudaSuccess) {
+        cudaFree(scratch);
+        return cuda_fail(e, "scratch copy");
+      }
+      target = scratch;
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    Prepared winner = plan->prep;
+    int rc = TTB_OK;
+    for (const Spec& sp : plan->cands) {
+      Prepared pr;
+      if (!prepare(plan->geo, sp, plan->sms, &pr, nullptr)) continue;
+      if (!aligned(A, pr.a_align) || !aligned(target, pr.b_align)) continue;
+      for (int i = 0; i < warmups && rc == TTB_OK; ++i)
+        if (launch(plan->geo, pr, A, target, s) != cudaSuccess) rc = TTB_ECUDA;
+      for (int i = 0; i < reps && rc == TTB_OK; ++i) {
+        cudaEventRecord(e0, s);
+        if (launch(plan->geo, pr, A, target, s) != cudaSuccess) rc = TTB_ECUDA;
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        // ties keep the earlier (heuristically better) candidate, like
+        // select_solution's cost tie-break (tuner.cpp:48-64)
+        if (ms < best) {
+          best = ms;
+          winner = pr;
+        }
+      }
+      if (rc) break;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (scratch) cudaFree(scratch);
+    if (rc) return cuda_fail(cudaGetLastError(), "autotune");
+    plan->prep = winner;
+    if (plan->cached) {
+      std::lock_guard<std::mutex> lk(g_mu);
+      g_choice[plan->key] = winner.spec.text();
+      g_plans.clear();  // one-shot plans re-plan and pick the tuned choice up
+    }
+    if (plan->orig.beta == 0.0) {  // leave B holding exactly one application
+      const int r2 = execute(plan, plan->prep, A, B, s, plan->orig.alpha, plan->orig.beta);
+      if (r2) return r2;
+    }
+    return ok();
+  });
+}
+
+int ttb_plan_describe(ttb_plan plan, char* buf, size_t len) {
+  if (!plan) return fail(TTB_EINVAL, "plan: null handle");
+  const std::string t = plan->prep.spec.text();
+  if (!buf || len <= t.size()) return fail(TTB_EINVAL, "describe: buffer too small");
+  std::memcpy(buf, t.c_str(), t.size() + 1);
+  return ok();
+}
+
+int ttb_plan_candidates(ttb_plan plan, char* buf, size_t len) {
+  if (!plan) return fail(TTB_EINVAL, "plan: null handle");
+  std::string t;
+  for (const Spec& s : plan->cands) t += s.text() + "\n";
+  if (!buf || len <= t.size()) return fail(TTB_EINVAL, "candidates: buffer too small");
+  std::memcpy(buf, t.c_str(), t.size() + 1);
+  return ok();
+}
+
+int ttb_plan_select(ttb_plan plan, const char* plan_text) {
+  if (!plan) return fail(TTB_EINVAL, "plan: null handle");
+  return guarded([&] {
+    Spec s;
+    if (!plan_text || !Spec::parse(plan_text, &s)) return fail(TTB_EINVAL, "plan: cannot parse plan text");
+    std::string why;
+    Prepared pr;
+    if (!prepare(plan->geo, s, plan->sms, &pr, &why)) return fail(TTB_EINVAL, "plan: " + why);
+    plan->prep = pr;
+    return ok();
+  });
+}
+
+int ttb_plan_launches(ttb_plan plan, int* launches_per_execute) {
+  if (!plan) return fail(TTB_EINVAL, "plan: null handle");
+  if (launches_per_execute) *launches_per_execute = 1;
+  return ok();
+}
+
+int ttb_fill_uniform(int kind, int rank, const int64_t* sizes, const int64_t* ld,
+                     const int64_t* origin, const int64_t* global_sizes, uint64_t seed, void* buf,
+                     ttb_stream stream) {
+  BoxParams bp;
+  int rc = box_params(kind, rank, sizes, ld, origin, global_sizes, &bp);
+  if (rc) return rc;
+  const cudaError_t e = launch_fill_uniform(kind_double(kind), bp, seed, buf,
+                                            reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? ok() : cuda_fail(e, "fill_uniform");
+}
+
+int ttb_fill_sentinel(int kind, int64_t elements, void* buf, ttb_stream stream) {
+  if (kind < 0 || kind > 3 || elements < 0) return fail(TTB_EINVAL, "sentinel: bad arguments");
+  const cudaError_t e = launch_fill_sentinel(kind_double(kind), elements * kind_components(kind), buf,
+                                             reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? ok() : cuda_fail(e, "fill_sentinel");
+}
+
+int ttb_checksum(int kind, int rank, const int64_t* sizes, const int64_t* ld,
+                 const int64_t* origin, const int64_t* global_sizes, const void* buf,
+                 uint64_t* out, ttb_stream stream) {
+  BoxParams bp;
+  int rc = box_params(kind, rank, sizes, ld, origin, global_sizes, &bp);
+  if (rc) return rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(*d), s);
+  if (e != cudaSuccess) return cuda_fail(e, "checksum alloc");
+  cudaMemsetAsync(d, 0, sizeof(*d), s);
+  e = launch_checksum(kind_double(kind), bp, buf, d, s);
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(d, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "checksum");
+  if (out) *out = h;
+  return ok();
+}
+
+uint64_t ttb_launch_count(void) { return ttb::launch_total(); }
+
+int ttb_debug_candidates(int kind_a, int kind_b, int rank, const int* perm, const int64_t* sizes,
+                         const int64_t* lda, const int64_t* ldb, double alpha, double beta,
+                         char* buf, size_t len) {
+  return guarded([&] {
+    const Problem p = from_args(kind_a, kind_b, rank, perm, sizes, lda, ldb, alpha, beta);
+    check(p);
+    const Merged m = fuse_indices(p);
+    std::string t;
+    for (const Spec& s : candidates(make_geo(m.p))) t += s.text() + "\n";
+    if (!buf || len <= t.size()) return fail(TTB_EINVAL, "candidates: buffer too small");
+    std::memcpy(buf, t.c_str(), t.size() + 1);
+    return ok();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,44 @@
+// launch.hpp -- host entry points into the templated kernels (kern_*.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "params.hpp"
+
+namespace ttb {
+
+// mode: 0 move (alpha == 1, beta == 0), 1 scale (beta == 0), 2 update (beta != 0)
+cudaError_t launch_copy(int ka, int kb, int v, int mode, const CopyParams& p, const Launch& l,
+                        cudaStream_t s);
+cudaError_t launch_rt(int ka, int kb, int mx, int my, int mode, const RtParams& p,
+                      const Launch& l, cudaStream_t s);
+cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
+                        cudaStream_t s);
+
+// resident CTAs per SM for a variant (cudaOccupancyMaxActiveBlocksPerMultiprocessor)
+int occupancy_copy(int ka, int kb, int v, int mode, int block);
+int occupancy_rt(int ka, int kb, int mx, int my, int mode, int block);
+int occupancy_smem(int ka, int kb, int mode, int block, int smem);
+
+// data utilities (util.cu)
+struct BoxParams {
+  int rank = 0;
+  int C = 1;
+  int64_t ext[16];
+  int64_t st[16];    // memory strides (elements)
+  int64_t gst[16];   // global logical strides
+  int64_t gbase = 0; // global logical index of the box origin
+  int64_t total = 1;
+};
+cudaError_t launch_fill_uniform(bool dbl, const BoxParams& p, uint64_t seed, void* buf,
+                                cudaStream_t s);
+cudaError_t launch_fill_sentinel(bool dbl, int64_t scalars, void* buf, cudaStream_t s);
+cudaError_t launch_checksum(bool dbl, const BoxParams& p, const void* buf,
+                            unsigned long long* dev_out, cudaStream_t s);
+
+// number of kernels launched by this library (ttb_launch_count)
+void count_launch();
+
+}  // namespace ttb

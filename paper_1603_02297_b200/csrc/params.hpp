@@ -1,0 +1,108 @@
+// params.hpp -- launch parameter blocks shared by the host planner and the
+// sm_100a kernels.  All in-kernel index spaces are 32-bit (the executor splits
+// problems whose spaces would not fit, see api.cpp); memory offsets are 64-bit.
+#pragma once
+
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define TTB_HD __host__ __device__ __forceinline__
+#else
+#define TTB_HD inline
+#endif
+
+namespace ttb {
+
+constexpr int kSpaceDims = 16;  // axes per flattened index space
+
+// Unsigned 32-bit division by a run-time constant: q = (umulhi(n, m) + n) >> s
+// (round-up multiplier; exact for every n < 2^32).
+struct Div32 {
+  uint32_t d = 1, m = 1, s = 0;
+
+  static Div32 make(uint32_t d) {
+    Div32 r;
+    r.d = d;
+    uint32_t s = 0;
+    while ((uint64_t{1} << s) < d) ++s;
+    r.s = s;
+    r.m = static_cast<uint32_t>(((uint64_t{1} << 32) * ((uint64_t{1} << s) - d)) / d + 1);
+    return r;
+  }
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t udiv(uint32_t n, const Div32& f) {
+  return static_cast<uint32_t>((static_cast<uint64_t>(__umulhi(n, f.m)) + n) >> f.s);
+}
+#endif
+
+// A group of tensor axes flattened column-major into one index (first axis
+// fastest), with each axis' element stride in A and in B.
+struct Space {
+  int nd = 0;
+  uint32_t total = 1;
+  Div32 ext[kSpaceDims];
+  int64_t sa[kSpaceDims];
+  int64_t sb[kSpaceDims];
+};
+
+enum Variant : int { kCopy = 0, kRt = 1, kSmem = 2 };
+
+// Element-wise update constants (the W-typed alpha/beta are formed in-kernel).
+struct Scale {
+  double alpha = 1.0, beta = 0.0;
+};
+
+// kCopy: rows of `lead` elements contiguous in both tensors (shared stride-1
+// index, run_case1 / run_copy_1d analogue), rows enumerated by `rows`.
+struct CopyParams {
+  const void* A;
+  void* B;
+  Scale sc;
+  Space rows;
+  uint32_t vec_per_row;   // lead / V
+  Div32 vpr;              // divisor vec_per_row
+  uint32_t total_vec;     // rows.total * vec_per_row
+};
+
+// kRt: register micro-tile transpose between the X space (starts with A's
+// stride-1 axis) and the Y space (starts with B's stride-1 axis), vectors of
+// MX elements along X on load and MY elements along Y on store.
+struct RtParams {
+  const void* A;
+  void* B;
+  Scale sc;
+  Space X, Y, O;
+  int lx;                 // lanes along X per warp (32/lx along Y)
+  uint32_t wx, wy;        // warp tile: lx*MX by (32/lx)*MY
+  uint32_t nxc, nyc;      // chunk counts along X / Y
+  Div32 dnx, dny;         // divisors nxc, nyc
+  int order;              // 0: X chunks fastest, 1: Y chunks fastest
+  uint32_t items;         // nxc * nyc * O.total
+  int64_t sa_y0;          // A stride of Y's first axis
+  int64_t sb_x0;          // B stride of X's first axis
+};
+
+// kSmem: shared-memory staged tile  S (shared lead) x TX x TY  with padded
+// rows of `rl` elements; per-tile offset tables live in shared memory too.
+struct SmemParams {
+  const void* A;
+  void* B;
+  Scale sc;
+  Space X, Y, O;
+  uint32_t S, tx, ty, rl;
+  Div32 dS, dtx, dty;
+  uint32_t nxc, nyc;
+  Div32 dnx, dny;
+  int order;
+  uint32_t items;
+};
+
+// Launch shape chosen by the planner.
+struct Launch {
+  int grid = 0, block = 256;
+  int smem = 0;
+};
+
+}  // namespace ttb

@@ -1,0 +1,507 @@
+// plan.cpp -- candidate generation and launch preparation for sm_100a.
+#include "plan.hpp"
+
+#include "launch.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+
+namespace ttb {
+
+namespace {
+
+constexpr uint64_t kIdxLimit = uint64_t{1} << 31;
+
+int mode_of(double alpha, double beta) {
+  if (beta != 0.0) return 2;
+  return alpha == 1.0 ? 0 : 1;
+}
+
+bool build_space(const Geo& g, const std::vector<int>& axes, Space* s) {
+  *s = Space{};
+  s->nd = static_cast<int>(axes.size());
+  uint64_t tot = 1;
+  for (size_t i = 0; i < axes.size(); ++i) {
+    const int a = axes[i];
+    s->ext[i] = Div32::make(static_cast<uint32_t>(g.n[a]));
+    s->sa[i] = g.sa[a];
+    s->sb[i] = g.sb[a];
+    tot *= static_cast<uint64_t>(g.n[a]);
+    if (tot >= kIdxLimit) return false;
+  }
+  s->total = static_cast<uint32_t>(tot);
+  return true;
+}
+
+int64_t prod(const Geo& g, const std::vector<int>& axes) {
+  int64_t p = 1;
+  for (int a : axes) p *= g.n[a];
+  return p;
+}
+
+// axes of the problem not in `used`, ordered by B position (outer tiles then
+// sweep B's memory order, which keeps consecutive CTAs' stores adjacent)
+std::vector<int> outer_axes(const Geo& g, const std::vector<int>& x, const std::vector<int>& y,
+                            int skip) {
+  std::vector<int> o;
+  for (int k = 0; k < g.r; ++k) {
+    const int a = g.at[k];
+    if (a == skip) continue;
+    if (std::find(x.begin(), x.end(), a) != x.end()) continue;
+    if (std::find(y.begin(), y.end(), a) != y.end()) continue;
+    o.push_back(a);
+  }
+  return o;
+}
+
+bool disjoint(const std::vector<int>& x, const std::vector<int>& y) {
+  for (int a : x)
+    if (std::find(y.begin(), y.end(), a) != y.end()) return false;
+  return true;
+}
+
+// X group: A axes [x0, x0+kx); Y group: B positions [y0, y0+ky)
+std::vector<int> x_group(int x0, int kx) {
+  std::vector<int> v;
+  for (int i = 0; i < kx; ++i) v.push_back(x0 + i);
+  return v;
+}
+std::vector<int> y_group(const Geo& g, int y0, int ky) {
+  std::vector<int> v;
+  for (int i = 0; i < ky; ++i) v.push_back(g.at[y0 + i]);
+  return v;
+}
+
+// grow the X group (A axes start, start+1, ...) and the Y group (B positions
+// start, start+1, ...) until each spans >= target elements or would overlap
+void choose_groups(const Geo& g, int start, int64_t tx_target, int64_t ty_target, int* kx,
+                   int* ky) {
+  const int y_first = g.at[start];
+  int k = 1;
+  while (start + k < g.r && start + k != y_first && prod(g, x_group(start, k)) < tx_target) ++k;
+  *kx = k;
+  const std::vector<int> xs = x_group(start, k);
+  int m = 1;
+  while (start + m < g.r) {
+    const int a = g.at[start + m];
+    if (std::find(xs.begin(), xs.end(), a) != xs.end()) break;
+    if (prod(g, y_group(g, start, m)) >= ty_target) break;
+    ++m;
+  }
+  *ky = m;
+}
+
+// largest vector width w (elements, power of two, w*ebytes <= cap) with
+// extent % w == 0 and every other stride % w == 0
+int vec_width(int64_t extent, const int64_t* strides, int r, int skip, int ebytes, int cap) {
+  for (int w = std::min(4, cap / ebytes); w > 1; w /= 2) {
+    if (extent % w) continue;
+    bool ok = true;
+    for (int a = 0; a < r && ok; ++a)
+      if (a != skip && strides[a] % w) ok = false;
+    if (ok) return w;
+  }
+  return 1;
+}
+
+// shared-memory bank simulation for the smem tile walks: wavefronts per warp
+// request summed over the first warps of the load (A-order) and store
+// (B-order) walks, for a candidate row length rl
+int smem_wavefronts(uint32_t S, uint32_t tx, uint32_t ty, uint32_t rl, int ebytes) {
+  const int words = ebytes / 4;                  // 1, 2 or 4 banks per element
+  const int lanes_per_phase = 32 / words;         // 128-byte shared-memory wavefront
+  const uint32_t L = S * tx * ty;
+  int total = 0;
+  for (int walk = 0; walk < 2; ++walk) {
+    for (uint32_t w = 0; w < 8; ++w) {
+      for (int ph = 0; ph < 32 / lanes_per_phase; ++ph) {
+        // distinct word addresses per bank within this phase
+        std::vector<std::vector<uint32_t>> bank(32);
+        for (int l = ph * lanes_per_phase; l < (ph + 1) * lanes_per_phase; ++l) {
+          const uint32_t f = w * 32 + static_cast<uint32_t>(l);
+          if (f >= L) continue;
+          const uint32_t s = f % S, r = f / S;
+          uint32_t x, y;
+          if (walk == 0) {
+            x = r % tx;
+            y = r / tx;
+          } else {
+            y = r % ty;
+            x = r / ty;
+          }
+          const uint32_t idx = y * rl + x * S + s;
+          for (int q = 0; q < words; ++q) {
+            const uint32_t wa = idx * static_cast<uint32_t>(words) + static_cast<uint32_t>(q);
+            auto& b = bank[wa % 32];
+            if (std::find(b.begin(), b.end(), wa) == b.end()) b.push_back(wa);
+          }
+        }
+        size_t deg = 0;
+        for (auto& b : bank) deg = std::max(deg, b.size());
+        total += static_cast<int>(std::max<size_t>(deg, 1));
+      }
+    }
+  }
+  return total;
+}
+
+uint32_t best_row_length(uint32_t S, uint32_t tx, uint32_t ty, int ebytes) {
+  const uint32_t base = S * tx;
+  uint32_t best = base;
+  int best_w = 1 << 30;
+  for (uint32_t pad = 0; pad < 32; ++pad) {
+    const int w = smem_wavefronts(S, tx, ty, base + pad, ebytes);
+    if (w < best_w) {
+      best_w = w;
+      best = base + pad;
+    }
+  }
+  return best;
+}
+
+}  // namespace
+
+Geo make_geo(const Problem& m) {
+  Geo g;
+  g.r = m.rank();
+  const std::vector<int64_t> sa = m.a_strides(), sb = m.b_strides_of_a();
+  for (int a = 0; a < g.r; ++a) {
+    g.n[a] = m.sizes[a];
+    g.sa[a] = sa[a];
+    g.sb[a] = sb[a];
+    g.pos[a] = m.perm[a] - 1;
+    g.at[m.perm[a] - 1] = a;
+  }
+  g.ka = m.kind_a;
+  g.kb = m.kind_b;
+  g.C = kind_components(m.kind_a);
+  g.eA = kind_bytes(m.kind_a);
+  g.eB = kind_bytes(m.kind_b);
+  g.alpha = m.alpha;
+  g.beta = m.beta;
+  g.mode = mode_of(m.alpha, m.beta);
+  g.elements = m.elements();
+  return g;
+}
+
+std::string Spec::text() const {
+  char buf[160];
+  switch (v) {
+    case kCopy: std::snprintf(buf, sizeof buf, "kern=copy;v=%d;occ=%d", w1, occ); break;
+    case kRt:
+      std::snprintf(buf, sizeof buf, "kern=rt;mx=%d;my=%d;lx=%d;kx=%d;ky=%d;order=%d;occ=%d", w1,
+                    w2, lx, kx, ky, order, occ);
+      break;
+    default:
+      std::snprintf(buf, sizeof buf, "kern=smem;kx=%d;ky=%d;tx=%d;ty=%d;order=%d;occ=%d", kx, ky,
+                    tx, ty, order, occ);
+  }
+  return buf;
+}
+
+bool Spec::parse(const std::string& s, Spec* out) {
+  Spec p;
+  std::stringstream ss(s);
+  std::string kv;
+  bool have_kern = false;
+  while (std::getline(ss, kv, ';')) {
+    const auto eq = kv.find('=');
+    if (eq == std::string::npos) return false;
+    const std::string k = kv.substr(0, eq), v = kv.substr(eq + 1);
+    if (k == "kern") {
+      have_kern = true;
+      if (v == "copy")
+        p.v = kCopy;
+      else if (v == "rt")
+        p.v = kRt;
+      else if (v == "smem")
+        p.v = kSmem;
+      else
+        return false;
+      continue;
+    }
+    char* end = nullptr;
+    const long x = std::strtol(v.c_str(), &end, 10);
+    if (!end || *end) return false;
+    if (k == "v" || k == "mx")
+      p.w1 = static_cast<int>(x);
+    else if (k == "my")
+      p.w2 = static_cast<int>(x);
+    else if (k == "lx")
+      p.lx = static_cast<int>(x);
+    else if (k == "kx")
+      p.kx = static_cast<int>(x);
+    else if (k == "ky")
+      p.ky = static_cast<int>(x);
+    else if (k == "tx")
+      p.tx = static_cast<int>(x);
+    else if (k == "ty")
+      p.ty = static_cast<int>(x);
+    else if (k == "order")
+      p.order = static_cast<int>(x);
+    else if (k == "occ")
+      p.occ = static_cast<int>(x);
+    else
+      return false;
+  }
+  if (!have_kern) return false;
+  *out = p;
+  return true;
+}
+
+std::vector<Spec> candidates(const Geo& g) {
+  std::vector<Spec> out;
+  const bool shared = g.pos[0] == 0;  // case 1 (or rank 1): A's stride-1 index stays stride-1
+  const int emax = std::max(g.eA, g.eB), emin = std::min(g.eA, g.eB);
+
+  if (shared) {
+    // --- copy kernel: whole columns of the shared index
+    int v = 1;
+    for (int w = std::min(4, 16 / emin); w > 1; w /= 2) {
+      if (w * emax > 32 || g.n[0] % w) continue;
+      bool ok = true;
+      for (int a = 1; a < g.r && ok; ++a)
+        if (g.sa[a] % w || g.sb[a] % w) ok = false;
+      if (ok) {
+        v = w;
+        break;
+      }
+    }
+    const int64_t lead_bytes = g.n[0] * emin;
+    const double cost = lead_bytes >= 128 ? 0.0 : (lead_bytes >= 32 ? 3.0 : 8.0);
+    for (int w = v; w >= 1; w /= 2) {
+      Spec s;
+      s.v = kCopy;
+      s.w1 = w;
+      s.cost = cost + (v / w) * 0.5;
+      out.push_back(s);
+    }
+  } else {
+    // --- register-transpose kernel
+    const int y_first = g.at[0];
+    const int mx = vec_width(g.n[0], g.sa, g.r, 0, g.eA, 16);
+    const int my = vec_width(g.n[y_first], g.sb, g.r, y_first, g.eB, 16);
+    for (int wxv : {mx, 1}) {
+      for (int wyv : {my, 1}) {
+        if ((wxv == 1 && mx != 1 && wyv == 1 && my != 1)) continue;
+        for (int lx : {2, 4, 8, 16}) {
+          const int ly = 32 / lx;
+          const int rowb = lx * wxv * g.eA, colb = ly * wyv * g.eB;
+          if (rowb < 32 || colb < 32) continue;
+          const int64_t wx = static_cast<int64_t>(lx) * wxv, wy = static_cast<int64_t>(ly) * wyv;
+          int kx, ky;
+          choose_groups(g, 0, std::max<int64_t>(wx * 4, 64), std::max<int64_t>(wy * 4, 64), &kx,
+                        &ky);
+          const std::vector<int> xs = x_group(0, kx), ys = y_group(g, 0, ky);
+          if (!disjoint(xs, ys)) continue;
+          const int64_t NX = prod(g, xs), NY = prod(g, ys);
+          const double ex = static_cast<double>(NX) / (((NX + wx - 1) / wx) * wx);
+          const double ey = static_cast<double>(NY) / (((NY + wy - 1) / wy) * wy);
+          Spec s;
+          s.v = kRt;
+          s.w1 = wxv;
+          s.w2 = wyv;
+          s.lx = lx;
+          s.kx = kx;
+          s.ky = ky;
+          const double eff = ex * ey;
+          s.cost = 1.0 + (1.0 - eff) * 12.0 + (std::min(rowb, colb) < 64 ? 1.5 : 0.0) +
+                   (wxv < mx ? 1.0 : 0.0) + (wyv < my ? 1.0 : 0.0) +
+                   std::fabs(std::log2(static_cast<double>(rowb) / colb)) * 0.1;
+          out.push_back(s);
+        }
+      }
+    }
+  }
+
+  // --- shared-memory staged tile (always applicable)
+  {
+    const int start = shared ? 1 : 0;
+    if (g.r > start || (shared && g.r == 1)) {
+      const uint32_t S = shared ? static_cast<uint32_t>(std::min<int64_t>(g.n[0], 1 << 20)) : 1;
+      if (!shared || g.r > 1) {
+        const int64_t budget = std::max<int64_t>(64, (16384 / g.eA) / S);
+        int kx, ky;
+        choose_groups(g, start, 64, 64, &kx, &ky);
+        const std::vector<int> xs = x_group(start, kx), ys = y_group(g, start, ky);
+        if (disjoint(xs, ys)) {
+          const int64_t NX = prod(g, xs), NY = prod(g, ys);
+          for (int64_t txp : {32, 64, 128, 256}) {
+            for (int64_t typ : {32, 64, 128, 256}) {
+              int64_t tx = std::min(NX, txp), ty = std::min(NY, typ);
+              if (tx * ty > budget * 2) continue;
+              // small sides: grow the other side to fill the tile
+              if (NY < typ) tx = std::min(NX, std::max<int64_t>(tx, budget / std::max<int64_t>(ty, 1)));
+              if (NX < txp) ty = std::min(NY, std::max<int64_t>(ty, budget / std::max<int64_t>(tx, 1)));
+              tx = std::min<int64_t>(tx, 1024);
+              ty = std::min<int64_t>(ty, 1024);
+              if (S * tx * ty > static_cast<int64_t>(48 * 1024 / g.eA)) continue;
+              bool dup = false;
+              for (const Spec& o : out)
+                if (o.v == kSmem && o.tx == tx && o.ty == ty) dup = true;
+              if (dup) continue;
+              Spec s;
+              s.v = kSmem;
+              s.kx = kx;
+              s.ky = ky;
+              s.tx = static_cast<int>(tx);
+              s.ty = static_cast<int>(ty);
+              const double fill = static_cast<double>(S * tx * ty * g.eA) / 16384.0;
+              const double exx = static_cast<double>(NX) / (((NX + tx - 1) / tx) * tx);
+              const double eyy = static_cast<double>(NY) / (((NY + ty - 1) / ty) * ty);
+              s.cost = 2.0 + std::fabs(std::log2(fill)) * 0.5 + (1.0 - exx * eyy) * 12.0 +
+                       (S * tx * g.eA < 128 ? 1.0 : 0.0) + (S * ty * g.eB < 128 ? 1.0 : 0.0);
+              out.push_back(s);
+            }
+          }
+        }
+      }
+    }
+  }
+  std::stable_sort(out.begin(), out.end(),
+                   [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
+  // the tile order alternative of the best two transposing candidates
+  std::vector<Spec> extra;
+  for (size_t i = 0; i < out.size() && extra.size() < 2; ++i)
+    if (out[i].v != kCopy) {
+      Spec s = out[i];
+      s.order = 1;
+      s.cost += 0.01;
+      extra.push_back(s);
+    }
+  out.insert(out.end(), extra.begin(), extra.end());
+  std::stable_sort(out.begin(), out.end(),
+                   [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
+  {
+    std::vector<Spec> uniq;
+    for (const Spec& s : out) {
+      bool dup = false;
+      for (const Spec& u : uniq) dup = dup || u.text() == s.text();
+      if (!dup) uniq.push_back(s);
+    }
+    out.swap(uniq);
+  }
+  // cap the list, keep an smem plan last as the alignment-free fallback
+  if (out.size() > 12) out.resize(12);
+  for (const Spec& s : out)
+    if (s.v == kSmem || (s.v == kCopy && s.w1 == 1)) {
+      out.push_back(s);
+      break;
+    }
+  return out;
+}
+
+bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* why) {
+  Prepared p;
+  p.spec = s;
+  p.mode = g.mode;
+  const Scale sc{g.alpha, g.beta};
+  const int occ_cap = s.occ > 0 ? s.occ : 64;
+  auto fail = [why](const char* m) {
+    if (why) *why = m;
+    return false;
+  };
+  if (s.v == kCopy) {
+    if (g.pos[0] != 0) return fail("copy: stride-1 index is transposed");
+    const int v = s.w1;
+    if (v < 1 || g.n[0] % v) return fail("copy: vector width does not divide the lead");
+    for (int a = 1; a < g.r; ++a)
+      if (g.sa[a] % v || g.sb[a] % v) return fail("copy: strides not vector aligned");
+    std::vector<int> rows;
+    for (int k = 1; k < g.r; ++k) rows.push_back(g.at[k]);
+    CopyParams& c = p.cp;
+    c.sc = sc;
+    if (!build_space(g, rows, &c.rows)) return fail("copy: index space exceeds 2^31");
+    c.vec_per_row = static_cast<uint32_t>(g.n[0] / v);
+    if (static_cast<uint64_t>(c.vec_per_row) * c.rows.total >= kIdxLimit)
+      return fail("copy: index space exceeds 2^31");
+    c.vpr = Div32::make(c.vec_per_row);
+    c.total_vec = c.vec_per_row * c.rows.total;
+    const int occ = std::min(occ_cap, std::max(1, occupancy_copy(g.ka, g.kb, v, g.mode, 256)));
+    const int64_t want = (static_cast<int64_t>(c.total_vec) + 256 * 4 - 1) / (256 * 4);
+    p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t{occ} * sms)));
+    p.a_align = v * g.eA;
+    p.b_align = v * g.eB;
+  } else if (s.v == kRt) {
+    if (g.pos[0] == 0) return fail("rt: stride-1 index is not transposed");
+    const int y_first = g.at[0];
+    const int mx = s.w1, my = s.w2;
+    if (mx * g.eA > 16 || my * g.eB > 16) return fail("rt: vector wider than 16 bytes");
+    if (g.n[0] % mx || g.n[y_first] % my) return fail("rt: vector width does not divide lead");
+    for (int a = 0; a < g.r; ++a) {
+      if (a != 0 && g.sa[a] % mx) return fail("rt: A strides not vector aligned");
+      if (a != y_first && g.sb[a] % my) return fail("rt: B strides not vector aligned");
+    }
+    if (s.lx < 1 || s.lx > 32 || (s.lx & (s.lx - 1))) return fail("rt: bad lane split");
+    const std::vector<int> xs = x_group(0, s.kx), ys = y_group(g, 0, s.ky);
+    if (s.kx < 1 || s.ky < 1 || s.kx > g.r || s.ky > g.r || !disjoint(xs, ys))
+      return fail("rt: X/Y groups overlap");
+    RtParams& r = p.rp;
+    r.sc = sc;
+    if (!build_space(g, xs, &r.X) || !build_space(g, ys, &r.Y) ||
+        !build_space(g, outer_axes(g, xs, ys, -1), &r.O))
+      return fail("rt: index space exceeds 2^31");
+    r.lx = s.lx;
+    r.wx = static_cast<uint32_t>(s.lx * mx);
+    r.wy = static_cast<uint32_t>((32 / s.lx) * my);
+    r.nxc = (r.X.total + r.wx - 1) / r.wx;
+    r.nyc = (r.Y.total + r.wy - 1) / r.wy;
+    r.dnx = Div32::make(r.nxc);
+    r.dny = Div32::make(r.nyc);
+    r.order = s.order;
+    const uint64_t items = uint64_t{r.nxc} * r.nyc * r.O.total;
+    if (items >= kIdxLimit) return fail("rt: too many tiles");
+    r.items = static_cast<uint32_t>(items);
+    r.sa_y0 = g.sa[y_first];
+    r.sb_x0 = g.sb[0];
+    const int occ = std::min(occ_cap, std::max(1, occupancy_rt(g.ka, g.kb, mx, my, g.mode, 256)));
+    const int64_t want = (static_cast<int64_t>(r.items) + 7) / 8;
+    p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t{occ} * sms)));
+    p.a_align = mx * g.eA;
+    p.b_align = my * g.eB;
+  } else {
+    const bool shared = g.pos[0] == 0;
+    const int start = shared ? 1 : 0;
+    if (g.r <= start) return fail("smem: nothing to transpose");
+    const std::vector<int> xs = x_group(start, s.kx), ys = y_group(g, start, s.ky);
+    if (s.kx < 1 || s.ky < 1 || start + s.kx > g.r || start + s.ky > g.r || !disjoint(xs, ys))
+      return fail("smem: X/Y groups overlap");
+    SmemParams& m = p.sp;
+    m.sc = sc;
+    if (!build_space(g, xs, &m.X) || !build_space(g, ys, &m.Y) ||
+        !build_space(g, outer_axes(g, xs, ys, shared ? 0 : -1), &m.O))
+      return fail("smem: index space exceeds 2^31");
+    m.S = shared ? static_cast<uint32_t>(g.n[0]) : 1;
+    if (s.tx < 1 || s.ty < 1) return fail("smem: empty tile");
+    m.tx = static_cast<uint32_t>(std::min<int64_t>(s.tx, m.X.total));
+    m.ty = static_cast<uint32_t>(std::min<int64_t>(s.ty, m.Y.total));
+    m.rl = best_row_length(m.S, m.tx, m.ty, g.eA);
+    m.dS = Div32::make(m.S);
+    m.dtx = Div32::make(m.tx);
+    m.dty = Div32::make(m.ty);
+    m.nxc = (m.X.total + m.tx - 1) / m.tx;
+    m.nyc = (m.Y.total + m.ty - 1) / m.ty;
+    m.dnx = Div32::make(m.nxc);
+    m.dny = Div32::make(m.nyc);
+    m.order = s.order;
+    const uint64_t items = uint64_t{m.nxc} * m.nyc * m.O.total;
+    if (items >= kIdxLimit) return fail("smem: too many tiles");
+    m.items = static_cast<uint32_t>(items);
+    const int64_t smem = static_cast<int64_t>(m.tx + m.ty) * 2 * 8 +
+                         static_cast<int64_t>(m.ty) * m.rl * g.eA;
+    if (smem > 200 * 1024) return fail("smem: tile too large");
+    p.l.smem = static_cast<int>(smem);
+    const int occ = std::min(occ_cap, std::max(1, occupancy_smem(g.ka, g.kb, g.mode, 256, p.l.smem)));
+    p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(m.items, int64_t{occ} * sms)));
+    p.a_align = std::min(16, g.eA);  // whole elements (Vec<SA, C>) move as a unit
+    p.b_align = std::min(16, g.eB);
+  }
+  p.l.block = 256;
+  *out = p;
+  return true;
+}
+
+}  // namespace ttb

@@ -1,0 +1,109 @@
+// shard.cpp -- multi-GPU partition of the output.
+//
+// Every element of B depends on exactly one element of A (executor.hpp:33-40),
+// so any partition of B's index space is independent: no exchange, no
+// collective on the data path.  Rank r receives a contiguous range of the
+// flattened index over B's k outermost positions, with k the smallest whose
+// extent product splits across `world` ranks within 5% of perfect balance.
+// The range decomposes into at most 2k-1 boxes of the original index space.
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/ttb.h"
+#include "problem.hpp"
+
+namespace {
+
+struct Box {
+  std::vector<int64_t> origin, extent;  // B position order
+};
+
+// boxes covering flattened range [lo, hi) over dims[d..] (slowest first)
+void split(const std::vector<int64_t>& ext, size_t d, int64_t lo, int64_t hi, Box cur,
+           std::vector<Box>& out) {
+  if (lo >= hi) return;
+  int64_t inner = 1;
+  for (size_t j = d + 1; j < ext.size(); ++j) inner *= ext[j];
+  if (d + 1 == ext.size()) {
+    cur.origin[d] = lo;
+    cur.extent[d] = hi - lo;
+    out.push_back(cur);
+    return;
+  }
+  int64_t a = lo / inner;
+  const int64_t b = hi / inner;
+  if (a == b) {
+    cur.origin[d] = a;
+    cur.extent[d] = 1;
+    split(ext, d + 1, lo - a * inner, hi - a * inner, cur, out);
+    return;
+  }
+  if (lo % inner) {
+    Box head = cur;
+    head.origin[d] = a;
+    head.extent[d] = 1;
+    split(ext, d + 1, lo % inner, inner, head, out);
+    ++a;
+  }
+  if (a < b) {
+    Box mid = cur;
+    mid.origin[d] = a;
+    mid.extent[d] = b - a;
+    for (size_t j = d + 1; j < ext.size(); ++j) {
+      mid.origin[j] = 0;
+      mid.extent[j] = ext[j];
+    }
+    out.push_back(mid);
+  }
+  if (hi % inner) {
+    Box tail = cur;
+    tail.origin[d] = b;
+    tail.extent[d] = 1;
+    split(ext, d + 1, 0, hi % inner, tail, out);
+  }
+}
+
+}  // namespace
+
+extern "C" int ttb_shard_boxes(int rank, const int* perm, const int64_t* sizes, int world, int r,
+                               int64_t* origins, int64_t* extents, int* n_boxes) {
+  if (rank < 1 || rank > 64 || !perm || !sizes || world < 1 || r < 0 || r >= world || !n_boxes)
+    return TTB_EINVAL;
+  std::vector<int> inv(static_cast<size_t>(rank), -1);
+  for (int a = 0; a < rank; ++a) {
+    if (perm[a] < 1 || perm[a] > rank || inv[static_cast<size_t>(perm[a] - 1)] >= 0) return TTB_EINVAL;
+    inv[static_cast<size_t>(perm[a] - 1)] = a;
+  }
+  // B extents, outermost first
+  std::vector<int64_t> outer;
+  int k = 0;
+  int64_t F = 1;
+  for (int p = rank - 1; p >= 0; --p) {
+    F *= sizes[inv[static_cast<size_t>(p)]];
+    outer.push_back(sizes[inv[static_cast<size_t>(p)]]);
+    ++k;
+    const int64_t per = (F + world - 1) / world;
+    if (static_cast<double>(per) * world / static_cast<double>(F) <= 1.05) break;
+  }
+  const int64_t lo = F * r / world, hi = F * (r + 1) / world;
+  Box base;
+  base.origin.assign(outer.size(), 0);
+  base.extent.assign(outer.size(), 0);
+  std::vector<Box> boxes;
+  split(outer, 0, lo, hi, base, boxes);
+  *n_boxes = static_cast<int>(boxes.size());
+  if (!origins || !extents) return TTB_OK;
+  for (size_t i = 0; i < boxes.size(); ++i) {
+    for (int a = 0; a < rank; ++a) {
+      origins[i * rank + a] = 0;
+      extents[i * rank + a] = sizes[a];
+    }
+    for (int j = 0; j < k; ++j) {
+      const int a = inv[static_cast<size_t>(rank - 1 - j)];
+      origins[i * rank + a] = boxes[i].origin[static_cast<size_t>(j)];
+      extents[i * rank + a] = boxes[i].extent[static_cast<size_t>(j)];
+    }
+  }
+  return TTB_OK;
+}

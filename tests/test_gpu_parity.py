@@ -1,0 +1,276 @@
+"""GPU parity: the sm_100a engine against the CPU oracle and the reference's
+golden outputs (needs a B200; run with -m gpu).
+
+Bar: bit-exact bytes of the WHOLE B buffer (padding included, as the
+reference's own tests compare, support.hpp:93-96) for every kind pair, every
+alpha/beta, every kernel variant the planner offers.  Full-size BASELINE
+configs are checked by u64 checksum against the reference's output
+(tests/golden/config_checksums.json, produced by the reference itself).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1603_02297_b200 as ttb  # noqa: E402
+from paper_1603_02297_b200.workloads import ALL, CONFIGS  # noqa: E402
+from golden_util import case_inputs, load_config_checksums, load_small_cases  # noqa: E402
+from oracle import COMPONENTS, SCALAR, kind_id  # noqa: E402
+from problems import b_sizes, random_problem  # noqa: E402
+
+PAIRS = [("s", "s"), ("d", "d"), ("c", "c"), ("z", "z"), ("s", "d"), ("d", "s"), ("c", "z"),
+         ("z", "c")]
+
+
+def _dev(x: np.ndarray):
+    return torch.from_numpy(x.copy()).cuda()
+
+
+def run_gpu(ka, kb, perm, sizes, lda, ldb, alpha, A, beta, B, plan_text=None):
+    p = ttb.make_problem(perm, sizes, ka, kb, alpha, beta, lda, ldb)
+    dA, dB = _dev(A), _dev(B)
+    if plan_text is None:
+        ttb.reference_transpose(
+            p, ttb.TensorBuffer(ka, A.size // COMPONENTS[kind_id(ka)], tensor=dA),
+            ttb.TensorBuffer(kb, B.size // COMPONENTS[kind_id(kb)], tensor=dB))
+    else:
+        plan = ttb.GpuPlan(p, cache=False)
+        plan.select(plan_text)
+        plan.execute(dA, dB)
+    torch.cuda.synchronize()
+    return dB.cpu().numpy()
+
+
+def all_plans(ka, kb, perm, sizes, lda, ldb, alpha, beta):
+    p = ttb.make_problem(perm, sizes, ka, kb, alpha, beta, lda, ldb)
+    return ttb.GpuPlan(p, cache=False).candidates()
+
+
+def test_golden_small_cases_every_variant(coracle):
+    """Reference outputs (tests/golden) reproduced bit for bit by every plan."""
+    meta, arrays = load_small_cases()
+    n_plans = 0
+    for case in meta:
+        A, B = case_inputs(coracle, case, arrays)
+        want = arrays[f"out{case['id']}"]
+        args = (case["kind_a"], case["kind_b"], case["perm"], case["sizes"], case["lda"],
+                case["ldb"])
+        got = run_gpu(*args, case["alpha"], A, case["beta"], B)
+        assert got.tobytes() == want.tobytes(), case
+        for text in all_plans(*args, case["alpha"], case["beta"]):
+            got = run_gpu(*args, case["alpha"], A, case["beta"], B, plan_text=text)
+            assert got.tobytes() == want.tobytes(), (case, text)
+            n_plans += 1
+    assert n_plans > len(meta)
+
+
+def _inputs(coracle, rng, ka, kb, perm, sizes, lda, ldb, beta):
+    na = coracle.required_elements_a(sizes, lda)
+    nb = coracle.required_elements_b(perm, sizes, ldb)
+    A = np.zeros(na * COMPONENTS[kind_id(ka)], SCALAR[kind_id(ka)])
+    B = np.zeros(nb * COMPONENTS[kind_id(kb)], SCALAR[kind_id(kb)])
+    coracle.fill_sentinel(ka, A)
+    coracle.fill_sentinel(kb, B)
+    coracle.fill_uniform(ka, sizes, lda, int(rng.integers(1 << 30)), A)
+    if beta != 0.0:
+        coracle.fill_uniform(kb, b_sizes(perm, sizes), ldb, int(rng.integers(1 << 30)), B)
+    return A, B
+
+
+@pytest.mark.parametrize("ka,kb", PAIRS)
+def test_random_problems_every_variant(coracle, ka, kb):
+    rng = np.random.default_rng(kind_id(ka) * 10 + kind_id(kb))
+    for t in range(24):
+        big = t % 3 == 0
+        perm, sizes, lda, ldb = random_problem(rng, 4 if big else 6, allow_padding=(t % 2 == 0),
+                                               allow_ones=not big, lo=(9 if big else None),
+                                               hi=(70 if big else None))
+        alpha, beta = [(1.0, 0.0), (1.3, 0.0), (0.7, 1.1), (2.0, 3.0)][t % 4]
+        A, B = _inputs(coracle, rng, ka, kb, perm, sizes, lda, ldb, beta)
+        want = B.copy()
+        coracle.transpose(ka, kb, perm, sizes, lda, ldb, alpha, A, beta, want)
+        for text in [None] + all_plans(ka, kb, perm, sizes, lda, ldb, alpha, beta):
+            got = run_gpu(ka, kb, perm, sizes, lda, ldb, alpha, A, beta, B, plan_text=text)
+            assert got.tobytes() == want.tobytes(), (perm, sizes, lda, ldb, alpha, beta, text)
+
+
+def test_device_generator_and_checksum_match_oracle(coracle):
+    for kind in "sdcz":
+        sizes, ld = [7, 5, 3], [9, 5, 4]
+        n = 9 * 5 * 4
+        h = np.zeros(n * COMPONENTS[kind_id(kind)], SCALAR[kind_id(kind)])
+        coracle.fill_sentinel(kind, h)
+        coracle.fill_uniform(kind, sizes, ld, 77, h, origin=[1, 2, 3], global_sizes=[10, 9, 8])
+        d = torch.from_numpy(np.zeros_like(h)).cuda()
+        ttb.fill_sentinel(kind, n, d.data_ptr())
+        ttb.fill_uniform(kind, sizes, ld, 77, d.data_ptr(), origin=[1, 2, 3],
+                         global_sizes=[10, 9, 8])
+        torch.cuda.synchronize()
+        assert d.cpu().numpy().tobytes() == h.tobytes()
+        assert ttb.checksum(kind, sizes, ld, d.data_ptr(), origin=[1, 2, 3],
+                            global_sizes=[10, 9, 8]) == \
+            coracle.checksum(kind, sizes, ld, h, origin=[1, 2, 3], global_sizes=[10, 9, 8])
+
+
+def _full_size(w, plan_text=None, autotune=False):
+    p = ttb.make_problem(w.perm, list(w.sizes), w.kind, w.kind, w.alpha, w.beta,
+                         w.lda and list(w.lda), w.ldb and list(w.ldb))
+    na, nb = ttb.required_elements_a(p), ttb.required_elements_b(p)
+    a = ttb.TensorBuffer(w.kind, na)
+    b = ttb.TensorBuffer(w.kind, nb)
+    ttb.fill_sentinel(w.kind, na, a.data_ptr())
+    ttb.fill_sentinel(w.kind, nb, b.data_ptr())
+    ttb.fill_uniform(w.kind, list(w.sizes), w.lda and list(w.lda), w.seed_a, a.data_ptr())
+    if w.beta != 0.0:
+        ttb.fill_uniform(w.kind, w.sizes_b, w.ldb and list(w.ldb), w.seed_b, b.data_ptr())
+    plan = ttb.GpuPlan(p, cache=False)
+    if plan_text:
+        plan.select(plan_text)
+    if autotune:
+        plan.autotune(a, b)   # beta != 0 tunes on scratch; beta == 0 leaves one application
+    else:
+        plan.execute(a, b)
+    ck = ttb.checksum(w.kind, w.sizes_b, w.ldb and list(w.ldb), b.data_ptr())
+    return ck, plan
+
+
+@pytest.mark.parametrize("w", CONFIGS, ids=[w.name for w in CONFIGS])
+def test_baseline_configs_match_reference_checksums(w):
+    golden = load_config_checksums()
+    ck, plan = _full_size(w)
+    assert ck == golden[w.name], plan.describe()
+    for text in plan.candidates()[:6]:
+        ck, _ = _full_size(w, plan_text=text)
+        assert ck == golden[w.name], text
+    ck, plan = _full_size(w, autotune=True)
+    assert ck == golden[w.name], plan.describe()
+
+
+@pytest.mark.slow
+def test_sweep_rows_match_reference_checksums():
+    golden = load_config_checksums()
+    for w in ALL[len(CONFIGS):]:
+        ck, plan = _full_size(w)
+        assert ck == golden[w.name], (w.name, plan.describe())
+        torch.cuda.empty_cache()
+
+
+def test_edge_cases(coracle):
+    rng = np.random.default_rng(3)
+    cases = [
+        ([1], [1009], None, None),                # rank 1 (executor.cpp:354-355)
+        ([1], [1], None, None),                   # single element
+        ([2, 1, 3], [1, 1, 1], None, None),       # all ones
+        ([1, 2, 3], [3, 4, 5], None, None),       # identity -> rank-1 copy
+        ([2, 1], [1, 7], None, None),             # size-1 dims
+        ([3, 1, 2], [37, 5, 6], [40, 5, 7], [5, 8, 37]),  # padded (test_executor.cpp:129-149)
+        ([1, 3, 2], [8, 6, 5], [9, 6, 5], [8, 5, 7]),     # padded case 1
+        ([2, 1], [1009, 7], None, None),          # primes
+        ([2, 1], [7, 1009], None, None),
+        ([6, 5, 4, 3, 2, 1], [3, 2, 5, 2, 3, 4], None, None),
+    ]
+    for (perm, sizes, lda, ldb) in cases:
+        for ka, kb in PAIRS:
+            for alpha, beta in [(1.0, 0.0), (2.5, 0.0), (2.0, 3.0), (0.0, 1.0)]:
+                A, B = _inputs(coracle, rng, ka, kb, perm, sizes, lda, ldb, beta)
+                want = B.copy()
+                coracle.transpose(ka, kb, perm, sizes, lda, ldb, alpha, A, beta, want)
+                got = run_gpu(ka, kb, perm, sizes, lda, ldb, alpha, A, beta, B)
+                assert got.tobytes() == want.tobytes(), (perm, sizes, ka, kb, alpha, beta)
+                if alpha == 0.0 and beta == 1.0:
+                    assert got.tobytes() == B.tobytes()
+
+
+def test_beta_zero_never_reads_b(coracle):
+    """B full of NaN must not leak into a beta == 0 result (executor.hpp:33-40)."""
+    rng = np.random.default_rng(4)
+    for perm, sizes in [([2, 1], [300, 200]), ([1, 3, 2], [64, 9, 70]), ([3, 2, 1], [4, 96, 40])]:
+        for text in all_plans("s", "s", perm, sizes, None, None, 1.3, 0.0):
+            A, B = _inputs(coracle, rng, "s", "s", perm, sizes, None, None, 0.0)
+            B[:] = np.nan
+            want = np.zeros_like(B)
+            coracle.transpose("s", "s", perm, sizes, None, None, 1.3, A, 0.0, want)
+            got = run_gpu("s", "s", perm, sizes, None, None, 1.3, A, 0.0, B, plan_text=text)
+            assert got.tobytes() == want.tobytes(), text
+
+
+def test_misaligned_buffers_take_the_fallback(coracle):
+    rng = np.random.default_rng(5)
+    perm, sizes = [2, 1], [64, 48]
+    p = ttb.make_problem(perm, sizes, "s", "s", 1.0, 0.0)
+    A, B = _inputs(coracle, rng, "s", "s", perm, sizes, None, None, 0.0)
+    want = B.copy()
+    coracle.transpose("s", "s", perm, sizes, None, None, 1.0, A, 0.0, want)
+    dA = torch.zeros(A.size + 1, dtype=torch.float32, device="cuda")
+    dB = torch.zeros(B.size + 1, dtype=torch.float32, device="cuda")
+    dA[1:] = torch.from_numpy(A).cuda()
+    dB[1:] = torch.from_numpy(B).cuda()
+    plan = ttb.GpuPlan(p, cache=False)
+    plan.execute(dA.data_ptr() + 4, dB.data_ptr() + 4)  # 4-byte aligned, not 16
+    torch.cuda.synchronize()
+    assert dB[1:].cpu().numpy().tobytes() == want.tobytes()
+
+
+def test_buffer_errors_match_reference_messages():
+    p = ttb.make_problem([2, 1], [8, 8])
+    a, b = ttb.make_buffer_a(p), ttb.make_buffer_b(p)
+    with pytest.raises(ValueError, match="A buffer: element kind mismatch"):
+        ttb.reference_transpose(p, ttb.TensorBuffer("d", 64), b)
+    with pytest.raises(ValueError, match="A buffer: too small for problem"):
+        ttb.reference_transpose(p, ttb.TensorBuffer("s", 63), b)
+    with pytest.raises(ValueError, match="B buffer: too small for problem"):
+        ttb.reference_transpose(p, a, ttb.TensorBuffer("s", 63))
+    with pytest.raises(ValueError, match="perm: not a permutation of 1..2"):
+        ttb.reference_transpose(ttb.make_problem([1, 1], [8, 8]), a, b)
+
+
+def test_sharded_execution_equals_single_call(coracle):
+    """1 rank vs P ranks: executing every rank's boxes gives the same bytes."""
+    rng = np.random.default_rng(6)
+    for perm, sizes, kind, beta in [([3, 1, 2], [30, 7, 9], "s", 0.0),
+                                    ([2, 4, 3, 6, 1, 5], [6, 4, 3, 9, 2, 5], "d", 0.5),
+                                    ([2, 1], [101, 37], "c", 0.0)]:
+        p = ttb.make_problem(perm, sizes, kind, kind, 1.0, beta)
+        A, B = _inputs(coracle, rng, kind, kind, perm, sizes, None, None, beta)
+        want = B.copy()
+        coracle.transpose(kind, kind, perm, sizes, None, None, 1.0, A, beta, want)
+        sa = ttb.element_strides_a(p)
+        sbA = ttb.element_strides_b_for_a(p)
+        esz = ttb.ElementKind.from_code(kind).bytes
+        for world in (2, 3, 8):
+            dA, dB = _dev(A), _dev(B)
+            for r in range(world):
+                for origin, ext in ttb.shard_boxes(p, world, r):
+                    q = ttb.make_problem(perm, ext, kind, kind, 1.0, beta, p.lda, p.ldb)
+                    offa = sum(o * s for o, s in zip(origin, sa)) * esz
+                    offb = sum(o * s for o, s in zip(origin, sbA)) * esz
+                    ttb.GpuPlan(q).execute(dA.data_ptr() + offa, dB.data_ptr() + offb)
+            torch.cuda.synchronize()
+            assert dB.cpu().numpy().tobytes() == want.tobytes(), (perm, world)
+
+
+def test_host_end_to_end_path(coracle):
+    rng = np.random.default_rng(8)
+    for perm, sizes, lda, ldb, beta in [([2, 1], [300, 200], None, None, 0.0),
+                                        ([3, 1, 2], [37, 5, 6], [40, 5, 7], [5, 8, 37], 0.0),
+                                        ([2, 3, 1], [33, 20, 7], None, None, 1.5)]:
+        A, B = _inputs(coracle, rng, "d", "d", perm, sizes, lda, ldb, beta)
+        want = B.copy()
+        coracle.transpose("d", "d", perm, sizes, lda, ldb, 0.5, A, beta, want)
+        plan = ttb.GpuPlan(ttb.make_problem(perm, sizes, "d", "d", 0.5, beta, lda, ldb))
+        got = B.copy()
+        plan.execute_host(A, got)
+        assert got.tobytes() == want.tobytes()
+
+
+def test_kernels_actually_launch():
+    before = ttb.launch_count()
+    p = ttb.make_problem([2, 1], [64, 64])
+    a, b = ttb.make_buffer_a(p), ttb.make_buffer_b(p)
+    ttb.reference_transpose(p, a, b)
+    torch.cuda.synchronize()
+    assert ttb.launch_count() == before + 1

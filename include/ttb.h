@@ -151,7 +151,8 @@ int ttb_plan_execute_host(ttb_plan plan, const void* A_host, void* B_host);
  * device buffers with CUDA events (warmups + reps, best-of, as
  * measure_candidate, tuner.cpp:27-46) and keep the fastest; the choice is
  * written back to the plan cache.  When beta != 0 the candidates run on a
- * plan-owned scratch copy so B receives no extra updates. */
+ * scratch copy of B.  On return B holds exactly one application of the tuned
+ * plan, as after ttb_plan_execute. */
 int ttb_plan_autotune(ttb_plan plan, const void* A, void* B, int warmups, int reps,
                       ttb_stream stream);
 

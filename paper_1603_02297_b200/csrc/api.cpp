@@ -429,10 +429,10 @@ int ttb_plan_autotune(ttb_plan plan, const void* A, void* B, int warmups, int re
       g_choice[plan->key] = winner.spec.text();
       g_plans.clear();  // one-shot plans re-plan and pick the tuned choice up
     }
-    if (plan->orig.beta == 0.0) {  // leave B holding exactly one application
-      const int r2 = execute(plan, plan->prep, A, B, s, plan->orig.alpha, plan->orig.beta);
-      if (r2) return r2;
-    }
+    // like a plain execute, leave B holding exactly one application (with
+    // beta == 0 every candidate overwrote it; with beta != 0 it is untouched)
+    const int r2 = execute(plan, plan->prep, A, B, s, plan->orig.alpha, plan->orig.beta);
+    if (r2) return r2;
     return ok();
   });
 }

@@ -7,10 +7,12 @@ namespace ttb {
 
 namespace {
 template <class F>
-cudaError_t with_smem(int ka, int kb, int mode, F&& f) {
+cudaError_t with_smem(int ka, int kb, int mode, bool dense, F&& f) {
   return with_types(ka, kb, [&](auto t) {
     using T = decltype(t);
     return with_mode(mode, [&](auto m) {
+      if (dense)
+        return f(&smem_dense_kernel<typename T::SA, typename T::SB, T::C, decltype(m)::value>);
       return f(&smem_kernel<typename T::SA, typename T::SB, T::C, decltype(m)::value>);
     });
   });
@@ -19,7 +21,7 @@ cudaError_t with_smem(int ka, int kb, int mode, F&& f) {
 
 cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                         cudaStream_t s) {
-  return with_smem(ka, kb, mode, [&](auto fn) {
+  return with_smem(ka, kb, mode, p.dense != 0, [&](auto fn) {
     if (l.smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
       if (e != cudaSuccess) return e;
@@ -30,9 +32,9 @@ cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Lau
   });
 }
 
-int occupancy_smem(int ka, int kb, int mode, int block, int smem) {
+int occupancy_smem(int ka, int kb, int mode, bool dense, int block, int smem) {
   int n = 0;
-  with_smem(ka, kb, mode, [&](auto fn) {
+  with_smem(ka, kb, mode, dense, [&](auto fn) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem);
   });

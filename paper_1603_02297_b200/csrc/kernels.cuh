@@ -190,15 +190,46 @@ __device__ __forceinline__ void decode(const Space& s, uint32_t idx, int64_t& oa
 
 // ------------------------------------------------------------- kernels --
 
-// Shared stride-1 index: each vector of V elements is contiguous in A and B.
+// Row r (tile-ordered linear row index) -> element offsets of the row start
+// in A and in B; false for the masked rows of partial tiles.
+__device__ __forceinline__ bool copy_row(const CopyParams& P, uint32_t r, int64_t& oa,
+                                         int64_t& ob) {
+  const uint32_t rit = r & ((1u << (P.ltx + P.lty)) - 1);
+  const uint32_t tile = r >> (P.ltx + P.lty);
+  uint32_t xc, yc, o;
+  if (P.order == 0) {
+    const uint32_t t = udiv(tile, P.dnx);
+    xc = tile - t * P.nxc;
+    o = udiv(t, P.dny);
+    yc = t - o * P.nyc;
+  } else {
+    const uint32_t t = udiv(tile, P.dny);
+    yc = tile - t * P.nyc;
+    o = udiv(t, P.dnx);
+    xc = t - o * P.nxc;
+  }
+  const uint32_t x = xc * P.tx + (rit & (P.tx - 1));
+  const uint32_t y = yc * P.ty + (rit >> P.ltx);
+  if (x >= P.X.total || y >= P.Y.total) return false;
+  int64_t a1, b1, a2, b2;
+  decode(P.O, o, oa, ob);
+  decode(P.X, x, a1, b1);
+  decode(P.Y, y, a2, b2);
+  oa += a1 + a2;
+  ob += b1 + b2;
+  return true;
+}
+
+// Shared stride-1 index, short rows: each thread moves vectors of V
+// elements, contiguous in A and B, U of them in flight.
 template <class SA, class SB, int C, int V, int MODE>
 __global__ void __launch_bounds__(256) copy_kernel(const CopyParams P) {
   const Update<SA, SB, MODE> up(P.sc);
   const SA* __restrict__ A = static_cast<const SA*>(P.A);
   SB* __restrict__ B = static_cast<SB*>(P.B);
-  constexpr int U = 4;  // independent vectors in flight per thread
+  constexpr int U = 4;
   const uint32_t nth = gridDim.x * blockDim.x;
-  for (uint32_t f0 = blockIdx.x * blockDim.x + threadIdx.x; f0 < P.total_vec; f0 += U * nth) {
+  for (uint32_t f0 = blockIdx.x * blockDim.x + threadIdx.x; f0 < P.items; f0 += U * nth) {
     Vec<SA, V * C> a[U];
     Vec<SB, V * C> b[U];
     SB* pb[U];
@@ -206,14 +237,15 @@ __global__ void __launch_bounds__(256) copy_kernel(const CopyParams P) {
     for (int u = 0; u < U; ++u) {
       const uint32_t f = f0 + u * nth;
       pb[u] = nullptr;
-      if (f < P.total_vec) {
-        const uint32_t row = udiv(f, P.vpr);
-        const uint32_t v = f - row * P.vec_per_row;
-        int64_t oa, ob;
-        decode(P.rows, row, oa, ob);
-        vload_a(a[u], A + (oa + static_cast<int64_t>(v) * V) * C);
-        pb[u] = B + (ob + static_cast<int64_t>(v) * V) * C;
-        if constexpr (MODE == 2) vload_b(b[u], pb[u]);
+      int64_t oa, ob;
+      if (f < P.items) {
+        const uint32_t row = udiv(f, P.dl);
+        const uint32_t v = f - row * P.lvec;
+        if (copy_row(P, row, oa, ob)) {
+          vload_a(a[u], A + (oa + static_cast<int64_t>(v) * V) * C);
+          pb[u] = B + (ob + static_cast<int64_t>(v) * V) * C;
+          if constexpr (MODE == 2) vload_b(b[u], pb[u]);
+        }
       }
     }
 #pragma unroll
@@ -226,56 +258,135 @@ __global__ void __launch_bounds__(256) copy_kernel(const CopyParams P) {
   }
 }
 
+// Shared stride-1 index, long rows: a warp streams one segment of 32*U
+// vectors of a row per item (row offsets decoded once per item).
+template <class SA, class SB, int C, int V, int MODE>
+__global__ void __launch_bounds__(256) copy_rows_kernel(const CopyParams P) {
+  const Update<SA, SB, MODE> up(P.sc);
+  const SA* __restrict__ A = static_cast<const SA*>(P.A);
+  SB* __restrict__ B = static_cast<SB*>(P.B);
+  constexpr int U = 8;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < P.items; it += nwarps) {
+    const uint32_t row = udiv(it, P.dseg);
+    const uint32_t seg = it - row * P.nseg;
+    int64_t oa, ob;
+    if (!copy_row(P, row, oa, ob)) continue;
+    const uint32_t v0 = seg * 32 * U + lane;
+    Vec<SA, V * C> a[U];
+    Vec<SB, V * C> b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t v = v0 + u * 32;
+      if (v < P.lvec) {
+        vload_a(a[u], A + (oa + static_cast<int64_t>(v) * V) * C);
+        if constexpr (MODE == 2) vload_b(b[u], B + (ob + static_cast<int64_t>(v) * V) * C);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t v = v0 + u * 32;
+      if (v < P.lvec) {
+#pragma unroll
+        for (int i = 0; i < V * C; ++i) b[u].v[i] = up(a[u].v[i], b[u].v[i]);
+        vstore(B + (ob + static_cast<int64_t>(v) * V) * C, b[u]);
+      }
+    }
+  }
+}
+
 // In-register micro-tile transpose.  A warp covers (lx*MX) x ((32/lx)*MY)
 // elements of the X-by-Y plane per item: lane (i, j) loads MY vectors of MX
 // elements (rows y..y+MY-1, contiguous in A), transposes them in registers
 // and stores MX vectors of MY elements (columns x..x+MX-1, contiguous in B).
 // The paper's w x w micro-kernel (executor.hpp:101-128) mapped to one thread.
+// Software-pipelined: the loads of a warp's next item are in flight while the
+// current item is transposed and stored, so HBM sees a continuous stream.
 template <class SA, class SB, int C, int MX, int MY, int MODE>
-__global__ void __launch_bounds__(256) rt_kernel(const RtParams P) {
+struct RtItem {
+  const SA* pa;
+  SB* pb;
+  bool valid;
+  Vec<SA, MX * C> r[MY];   // MY rows of MX elements (A side)
+  Vec<SB, MY * C> w[MX];   // MX columns of MY elements (B side; loaded when beta != 0)
+};
+
+template <class SA, class SB, int C, int MX, int MY, int MODE>
+__device__ __forceinline__ void rt_fetch(const RtParams& P, uint32_t it, uint32_t li, uint32_t lj,
+                                         RtItem<SA, SB, C, MX, MY, MODE>& I) {
+  uint32_t xc, yc, o;
+  if (P.order == 0) {
+    const uint32_t t = udiv(it, P.dnx);
+    xc = it - t * P.nxc;
+    o = udiv(t, P.dny);
+    yc = t - o * P.nyc;
+  } else {
+    const uint32_t t = udiv(it, P.dny);
+    yc = it - t * P.nyc;
+    o = udiv(t, P.dnx);
+    xc = t - o * P.nxc;
+  }
+  const uint32_t x = xc * P.wx + li * MX;
+  const uint32_t y = yc * P.wy + lj * MY;
+  I.valid = x < P.X.total && y < P.Y.total;
+  if (!I.valid) return;
+  int64_t aO, bO, aX, bX, aY, bY;
+  decode(P.O, o, aO, bO);
+  decode(P.X, x, aX, bX);
+  decode(P.Y, y, aY, bY);
+  I.pa = static_cast<const SA*>(P.A) + (aO + aX + aY) * C;
+  I.pb = static_cast<SB*>(P.B) + (bO + bX + bY) * C;
+#pragma unroll
+  for (int k = 0; k < MY; ++k) vload_a(I.r[k], I.pa + k * P.sa_y0 * C);
+  if constexpr (MODE == 2) {
+#pragma unroll
+    for (int j = 0; j < MX; ++j) vload_b(I.w[j], I.pb + j * P.sb_x0 * C);
+  }
+}
+
+template <class SA, class SB, int C, int MX, int MY, int MODE>
+__device__ __forceinline__ void rt_commit(const RtParams& P, const Update<SA, SB, MODE>& up,
+                                          RtItem<SA, SB, C, MX, MY, MODE>& I) {
+  if (!I.valid) return;
+#pragma unroll
+  for (int j = 0; j < MX; ++j) {
+#pragma unroll
+    for (int k = 0; k < MY; ++k)
+#pragma unroll
+      for (int c = 0; c < C; ++c) I.w[j].v[k * C + c] = up(I.r[k].v[j * C + c], I.w[j].v[k * C + c]);
+    vstore(I.pb + j * P.sb_x0 * C, I.w[j]);
+  }
+}
+
+template <class SA, class SB, int C, int MX, int MY, int MODE>
+__global__ void __launch_bounds__(256, 4) rt_kernel(const RtParams P) {
+  using Item = RtItem<SA, SB, C, MX, MY, MODE>;
   const Update<SA, SB, MODE> up(P.sc);
-  const SA* __restrict__ A = static_cast<const SA*>(P.A);
-  SB* __restrict__ B = static_cast<SB*>(P.B);
   const int lane = threadIdx.x & 31;
-  const uint32_t li = static_cast<uint32_t>(lane % P.lx);
-  const uint32_t lj = static_cast<uint32_t>(lane / P.lx);
+  const uint32_t li = static_cast<uint32_t>(lane & (P.lx - 1));
+  const uint32_t lj = static_cast<uint32_t>(lane >> P.lx_log2);
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < P.items; it += nwarps) {
-    uint32_t xc, yc, o;
-    if (P.order == 0) {
-      const uint32_t t = udiv(it, P.dnx);
-      xc = it - t * P.nxc;
-      o = udiv(t, P.dny);
-      yc = t - o * P.nyc;
-    } else {
-      const uint32_t t = udiv(it, P.dny);
-      yc = it - t * P.nyc;
-      o = udiv(t, P.dnx);
-      xc = t - o * P.nxc;
+  uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (it >= P.items) return;
+  Item a, b;
+  rt_fetch(P, it, li, lj, a);
+  // ping-pong between two register sets: fetch(next) overlaps commit(current)
+  for (;;) {
+    it += nwarps;
+    if (it >= P.items) {
+      rt_commit(P, up, a);
+      return;
     }
-    const uint32_t x = xc * P.wx + li * MX;
-    const uint32_t y = yc * P.wy + lj * MY;
-    if (x >= P.X.total || y >= P.Y.total) continue;
-    int64_t aO, bO, aX, bX, aY, bY;
-    decode(P.O, o, aO, bO);
-    decode(P.X, x, aX, bX);
-    decode(P.Y, y, aY, bY);
-    const SA* pa = A + (aO + aX + aY) * C;
-    Vec<SA, MX * C> r[MY];
-#pragma unroll
-    for (int k = 0; k < MY; ++k) vload_a(r[k], pa + k * P.sa_y0 * C);
-    SB* pb = B + (bO + bX + bY) * C;
-#pragma unroll
-    for (int j = 0; j < MX; ++j) {
-      Vec<SB, MY * C> w;
-      SB* q = pb + j * P.sb_x0 * C;
-      if constexpr (MODE == 2) vload_b(w, q);
-#pragma unroll
-      for (int k = 0; k < MY; ++k)
-#pragma unroll
-        for (int c = 0; c < C; ++c) w.v[k * C + c] = up(r[k].v[j * C + c], w.v[k * C + c]);
-      vstore(q, w);
+    rt_fetch(P, it, li, lj, b);
+    rt_commit(P, up, a);
+    it += nwarps;
+    if (it >= P.items) {
+      rt_commit(P, up, b);
+      return;
     }
+    rt_fetch(P, it, li, lj, a);
+    rt_commit(P, up, b);
   }
 }
 
@@ -375,6 +486,106 @@ __global__ void __launch_bounds__(256) smem_kernel(const SmemParams P) {
             if constexpr (MODE == 2) vload_b(w[u], q[u]);
             a[u] = tile[y * P.rl + x * P.S + s];
           }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!q[u]) continue;
+#pragma unroll
+        for (int c = 0; c < C; ++c) w[u].v[c] = up(a[u].v[c], w[u].v[c]);
+        vstore(q[u], w[u]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace ttb
+
+namespace ttb {
+
+// Dense fast path of the staged tile (the common case after index merging):
+// no shared stride-1 index, the X group is one contiguous run of A and the Y
+// group one contiguous run of B, tile extents are powers of two.  Per tile the
+// A offset of every row (y) and the B offset of every column (x) go to shared
+// memory; each element then costs a mask, a shift and one warp-broadcast
+// table read on either walk -- no division.
+template <class SA, class SB, int C, int MODE>
+__global__ void __launch_bounds__(256) smem_dense_kernel(const SmemParams P) {
+  using E = Vec<SA, C>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int64_t* rowA = reinterpret_cast<int64_t*>(smem_raw);  // [ty]: A offset of (x0, y0 + y)
+  int64_t* colB = rowA + P.ty;                            // [tx]: B offset of (x0 + x, y0)
+  E* tile = reinterpret_cast<E*>(colB + P.tx);
+
+  const Update<SA, SB, MODE> up(P.sc);
+  const SA* __restrict__ A = static_cast<const SA*>(P.A);
+  SB* __restrict__ B = static_cast<SB*>(P.B);
+  const uint32_t L = P.tx * P.ty;
+  const uint32_t mx = P.tx - 1, my = P.ty - 1;
+
+  for (uint32_t it = blockIdx.x; it < P.items; it += gridDim.x) {
+    uint32_t xc, yc, o;
+    if (P.order == 0) {
+      const uint32_t t = udiv(it, P.dnx);
+      xc = it - t * P.nxc;
+      o = udiv(t, P.dny);
+      yc = t - o * P.nyc;
+    } else {
+      const uint32_t t = udiv(it, P.dny);
+      yc = it - t * P.nyc;
+      o = udiv(t, P.dnx);
+      xc = t - o * P.nxc;
+    }
+    const uint32_t x0 = xc * P.tx, y0 = yc * P.ty;
+    const uint32_t nx = min(P.tx, P.X.total - x0), ny = min(P.ty, P.Y.total - y0);
+    int64_t aO, bO;
+    decode(P.O, o, aO, bO);
+    for (uint32_t i = threadIdx.x; i < ny; i += blockDim.x) {
+      int64_t a, b;
+      decode(P.Y, y0 + i, a, b);
+      rowA[i] = a + aO + x0;
+    }
+    for (uint32_t i = threadIdx.x; i < nx; i += blockDim.x) {
+      int64_t a, b;
+      decode(P.X, x0 + i, a, b);
+      colB[i] = b + bO + y0;
+    }
+    __syncthreads();
+
+    constexpr int U = 8;
+    for (uint32_t f0 = threadIdx.x; f0 < L; f0 += U * blockDim.x) {
+      E v[U];
+      int dst[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t f = f0 + u * blockDim.x;
+        const uint32_t x = f & mx, y = f >> P.ltx;
+        dst[u] = -1;
+        if (f < L && x < nx && y < ny) {
+          vload_a(v[u], A + (rowA[y] + x) * C);
+          dst[u] = static_cast<int>(y * P.rl + x);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (dst[u] >= 0) tile[dst[u]] = v[u];
+    }
+    __syncthreads();
+
+    for (uint32_t f0 = threadIdx.x; f0 < L; f0 += U * blockDim.x) {
+      Vec<SB, C> w[U];
+      E a[U];
+      SB* q[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t f = f0 + u * blockDim.x;
+        const uint32_t y = f & my, x = f >> P.lty;
+        q[u] = nullptr;
+        if (f < L && x < nx && y < ny) {
+          q[u] = B + (colB[x] + y) * C;
+          if constexpr (MODE == 2) vload_b(w[u], q[u]);
+          a[u] = tile[y * P.rl + x];
         }
       }
 #pragma unroll

@@ -56,14 +56,24 @@ struct Scale {
 
 // kCopy: rows of `lead` elements contiguous in both tensors (shared stride-1
 // index, run_case1 / run_copy_1d analogue), rows enumerated by `rows`.
+// Rows are enumerated in tiles of tx x ty rows over the X group (A axes after
+// the shared one) and the Y group (B positions after it), so both the reads
+// and the writes of neighbouring rows stay in a small address window.
 struct CopyParams {
   const void* A;
   void* B;
   Scale sc;
-  Space rows;
-  uint32_t vec_per_row;   // lead / V
-  Div32 vpr;              // divisor vec_per_row
-  uint32_t total_vec;     // rows.total * vec_per_row
+  Space X, Y, O;
+  uint32_t lvec;          // vectors per row (lead / V)
+  Div32 dl;               // divisor lvec
+  uint32_t tx, ty, ltx, lty;  // row tile, powers of two
+  uint32_t nxc, nyc;
+  Div32 dnx, dny;
+  int order;
+  uint32_t nseg;          // row segments of 32*U vectors (long-row kernel)
+  Div32 dseg;
+  uint32_t items;         // long rows: warp items; short rows: vectors (incl. masked)
+  int long_rows;          // 1: copy_rows_kernel, 0: copy_kernel
 };
 
 // kRt: register micro-tile transpose between the X space (starts with A's
@@ -74,7 +84,8 @@ struct RtParams {
   void* B;
   Scale sc;
   Space X, Y, O;
-  int lx;                 // lanes along X per warp (32/lx along Y)
+  int lx;                 // lanes along X per warp (32/lx along Y), power of two
+  int lx_log2;
   uint32_t wx, wy;        // warp tile: lx*MX by (32/lx)*MY
   uint32_t nxc, nyc;      // chunk counts along X / Y
   Div32 dnx, dny;         // divisors nxc, nyc
@@ -97,6 +108,10 @@ struct SmemParams {
   Div32 dnx, dny;
   int order;
   uint32_t items;
+  // dense fast path: S == 1, X contiguous in A, Y contiguous in B, tx/ty powers
+  // of two -> the walks need shifts and masks only, no per-element division
+  int dense;
+  uint32_t ltx, lty;
 };
 
 // Launch shape chosen by the planner.

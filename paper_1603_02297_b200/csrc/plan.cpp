@@ -162,6 +162,83 @@ uint32_t best_row_length(uint32_t S, uint32_t tx, uint32_t ty, int ebytes) {
   return best;
 }
 
+int64_t pow2_ceil(int64_t v) {
+  int64_t p = 1;
+  while (p < v) p *= 2;
+  return p;
+}
+
+bool x_dense_in_a(const Geo& g, const std::vector<int>& xs) {
+  if (xs.empty() || g.sa[xs[0]] != 1) return false;
+  for (size_t i = 0; i + 1 < xs.size(); ++i)
+    if (g.sa[xs[i + 1]] != g.sa[xs[i]] * g.n[xs[i]]) return false;
+  return true;
+}
+
+bool y_dense_in_b(const Geo& g, const std::vector<int>& ys) {
+  if (ys.empty() || g.sb[ys[0]] != 1) return false;
+  for (size_t i = 0; i + 1 < ys.size(); ++i)
+    if (g.sb[ys[i + 1]] != g.sb[ys[i]] * g.n[ys[i]]) return false;
+  return true;
+}
+
+// staged-tile candidates over every admissible pair of X / Y groups
+void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
+  const int start = shared ? 1 : 0;
+  if (g.r <= start) return;
+  const int64_t S = shared ? g.n[0] : 1;
+  if (S * 2 * 2 * g.eA > 48 * 1024) return;  // even a 2 x 2 tile would not fit
+  const int y_first = g.at[start];
+  std::vector<Spec> cand;
+  for (int kx = 1; start + kx <= g.r; ++kx) {
+    const std::vector<int> xs = x_group(start, kx);
+    if (std::find(xs.begin(), xs.end(), y_first) != xs.end()) break;
+    for (int ky = 1; start + ky <= g.r; ++ky) {
+      const std::vector<int> ys = y_group(g, start, ky);
+      if (!disjoint(xs, ys)) break;
+      const int64_t NX = prod(g, xs), NY = prod(g, ys);
+      if (NX >= int64_t{1} << 31 || NY >= int64_t{1} << 31) break;
+      const bool dense = !shared && x_dense_in_a(g, xs) && y_dense_in_b(g, ys);
+      std::vector<int64_t> txs, tys;
+      if (dense) {  // powers of two, capped at the group extent rounded up
+        for (int64_t t = 1; t <= std::min<int64_t>(1024, pow2_ceil(NX)); t *= 2) txs.push_back(t);
+        for (int64_t t = 1; t <= std::min<int64_t>(1024, pow2_ceil(NY)); t *= 2) tys.push_back(t);
+      } else {
+        for (int64_t t : {8, 16, 32, 64, 128, 256})
+          if (t < NX) txs.push_back(t);
+        txs.push_back(std::min<int64_t>(NX, 1024));
+        for (int64_t t : {8, 16, 32, 64, 128, 256})
+          if (t < NY) tys.push_back(t);
+        tys.push_back(std::min<int64_t>(NY, 1024));
+      }
+      for (int64_t tx : txs) {
+        for (int64_t ty : tys) {
+          const int64_t bytes = S * tx * ty * g.eA;
+          if (bytes < 4096 && !(tx >= NX && ty >= NY)) continue;
+          if (bytes > 40 * 1024) continue;
+          const double ex = static_cast<double>(NX) / (((NX + tx - 1) / tx) * tx);
+          const double ey = static_cast<double>(NY) / (((NY + ty - 1) / ty) * ty);
+          const int64_t run_a = S * std::min(tx, NX) * g.eA, run_b = S * std::min(ty, NY) * g.eB;
+          Spec s;
+          s.v = kSmem;
+          s.kx = kx;
+          s.ky = ky;
+          s.tx = static_cast<int>(tx);
+          s.ty = static_cast<int>(ty);
+          s.cost = 2.0 + (1.0 - ex * ey) * 12.0 + (run_a < 256 ? (run_a < 128 ? 2.0 : 1.0) : 0.0) +
+                   (run_b < 256 ? (run_b < 128 ? 2.0 : 1.0) : 0.0) +
+                   std::fabs(std::log2(static_cast<double>(bytes) / 16384.0)) * 0.3 +
+                   (dense ? 0.0 : 1.0) + 0.05 * (kx + ky);
+          cand.push_back(s);
+        }
+      }
+    }
+  }
+  std::stable_sort(cand.begin(), cand.end(),
+                   [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
+  for (size_t i = 0; i < cand.size() && i < 8; ++i) out->push_back(cand[i]);
+}
+
 }  // namespace
 
 Geo make_geo(const Problem& m) {
@@ -190,7 +267,10 @@ Geo make_geo(const Problem& m) {
 std::string Spec::text() const {
   char buf[160];
   switch (v) {
-    case kCopy: std::snprintf(buf, sizeof buf, "kern=copy;v=%d;occ=%d", w1, occ); break;
+    case kCopy:
+      std::snprintf(buf, sizeof buf, "kern=copy;v=%d;kx=%d;ky=%d;tx=%d;ty=%d;order=%d;occ=%d", w1,
+                    kx, ky, tx, ty, order, occ);
+      break;
     case kRt:
       std::snprintf(buf, sizeof buf, "kern=rt;mx=%d;my=%d;lx=%d;kx=%d;ky=%d;order=%d;occ=%d", w1,
                     w2, lx, kx, ky, order, occ);
@@ -272,12 +352,27 @@ std::vector<Spec> candidates(const Geo& g) {
     }
     const int64_t lead_bytes = g.n[0] * emin;
     const double cost = lead_bytes >= 128 ? 0.0 : (lead_bytes >= 32 ? 3.0 : 8.0);
+    // rows tiled over (A axis 1) x (B position 1): both streams stay local
+    const int ky = (g.r > 1 && g.at[1] != 1) ? 1 : 0;
+    const int64_t nx = g.r > 1 ? g.n[1] : 1, ny = ky ? g.n[g.at[1]] : 1;
+    const int64_t row_bytes = g.n[0] * emax;
     for (int w = v; w >= 1; w /= 2) {
-      Spec s;
-      s.v = kCopy;
-      s.w1 = w;
-      s.cost = cost + (v / w) * 0.5;
-      out.push_back(s);
+      for (auto t : {std::pair<int, int>{1, 1}, {8, 8}, {4, 16}, {16, 4}, {32, 1}, {2, 2}}) {
+        const int tx = static_cast<int>(std::min<int64_t>(t.first, pow2_ceil(nx)));
+        const int ty = ky ? static_cast<int>(std::min<int64_t>(t.second, pow2_ceil(ny))) : 1;
+        Spec s;
+        s.v = kCopy;
+        s.w1 = w;
+        s.kx = g.r > 1 ? 1 : 0;
+        s.ky = ky;
+        s.tx = tx;
+        s.ty = ty;
+        // tiles ~32 KB of rows keep reads and writes in small windows
+        const double tile_kb = static_cast<double>(tx) * ty * row_bytes / 1024.0;
+        s.cost = cost + (v / w) * 0.5 + (tx * ty == 1 ? 0.3 : 0.0) +
+                 std::fabs(std::log2(std::max(tile_kb, 1.0) / 32.0)) * 0.05;
+        out.push_back(s);
+      }
     }
   } else {
     // --- register-transpose kernel
@@ -318,49 +413,7 @@ std::vector<Spec> candidates(const Geo& g) {
   }
 
   // --- shared-memory staged tile (always applicable)
-  {
-    const int start = shared ? 1 : 0;
-    if (g.r > start || (shared && g.r == 1)) {
-      const uint32_t S = shared ? static_cast<uint32_t>(std::min<int64_t>(g.n[0], 1 << 20)) : 1;
-      if (!shared || g.r > 1) {
-        const int64_t budget = std::max<int64_t>(64, (16384 / g.eA) / S);
-        int kx, ky;
-        choose_groups(g, start, 64, 64, &kx, &ky);
-        const std::vector<int> xs = x_group(start, kx), ys = y_group(g, start, ky);
-        if (disjoint(xs, ys)) {
-          const int64_t NX = prod(g, xs), NY = prod(g, ys);
-          for (int64_t txp : {32, 64, 128, 256}) {
-            for (int64_t typ : {32, 64, 128, 256}) {
-              int64_t tx = std::min(NX, txp), ty = std::min(NY, typ);
-              if (tx * ty > budget * 2) continue;
-              // small sides: grow the other side to fill the tile
-              if (NY < typ) tx = std::min(NX, std::max<int64_t>(tx, budget / std::max<int64_t>(ty, 1)));
-              if (NX < txp) ty = std::min(NY, std::max<int64_t>(ty, budget / std::max<int64_t>(tx, 1)));
-              tx = std::min<int64_t>(tx, 1024);
-              ty = std::min<int64_t>(ty, 1024);
-              if (S * tx * ty > static_cast<int64_t>(48 * 1024 / g.eA)) continue;
-              bool dup = false;
-              for (const Spec& o : out)
-                if (o.v == kSmem && o.tx == tx && o.ty == ty) dup = true;
-              if (dup) continue;
-              Spec s;
-              s.v = kSmem;
-              s.kx = kx;
-              s.ky = ky;
-              s.tx = static_cast<int>(tx);
-              s.ty = static_cast<int>(ty);
-              const double fill = static_cast<double>(S * tx * ty * g.eA) / 16384.0;
-              const double exx = static_cast<double>(NX) / (((NX + tx - 1) / tx) * tx);
-              const double eyy = static_cast<double>(NY) / (((NY + ty - 1) / ty) * ty);
-              s.cost = 2.0 + std::fabs(std::log2(fill)) * 0.5 + (1.0 - exx * eyy) * 12.0 +
-                       (S * tx * g.eA < 128 ? 1.0 : 0.0) + (S * ty * g.eB < 128 ? 1.0 : 0.0);
-              out.push_back(s);
-            }
-          }
-        }
-      }
-    }
-  }
+  smem_candidates(g, shared, &out);
   std::stable_sort(out.begin(), out.end(),
                    [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
   // the tile order alternative of the best two transposing candidates
@@ -384,13 +437,17 @@ std::vector<Spec> candidates(const Geo& g) {
     }
     out.swap(uniq);
   }
-  // cap the list, keep an smem plan last as the alignment-free fallback
-  if (out.size() > 12) out.resize(12);
+  // cap the list, keep an element-aligned plan last as the fallback for
+  // misaligned buffers
+  Spec fallback;
+  bool have_fb = false;
   for (const Spec& s : out)
-    if (s.v == kSmem || (s.v == kCopy && s.w1 == 1)) {
-      out.push_back(s);
-      break;
+    if (!have_fb && (s.v == kSmem || (s.v == kCopy && s.w1 == 1))) {
+      fallback = s;
+      have_fb = true;
     }
+  if (out.size() > 16) out.resize(16);
+  if (have_fb) out.push_back(fallback);
   return out;
 }
 
@@ -410,18 +467,42 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     if (v < 1 || g.n[0] % v) return fail("copy: vector width does not divide the lead");
     for (int a = 1; a < g.r; ++a)
       if (g.sa[a] % v || g.sb[a] % v) return fail("copy: strides not vector aligned");
-    std::vector<int> rows;
-    for (int k = 1; k < g.r; ++k) rows.push_back(g.at[k]);
+    if (s.kx < 0 || s.ky < 0 || s.kx > 1 || s.ky > 1) return fail("copy: bad row groups");
+    if (s.kx == 0 && g.r > 1) return fail("copy: rows need the X group");
+    const std::vector<int> xs = s.kx ? std::vector<int>{1} : std::vector<int>{};
+    const std::vector<int> ys = s.ky ? std::vector<int>{g.at[1]} : std::vector<int>{};
+    if (s.ky && !disjoint(xs, ys)) return fail("copy: X/Y groups overlap");
+    const int tx = std::max(1, s.tx), ty = std::max(1, s.ty);
+    if ((tx & (tx - 1)) || (ty & (ty - 1))) return fail("copy: tile not a power of two");
     CopyParams& c = p.cp;
     c.sc = sc;
-    if (!build_space(g, rows, &c.rows)) return fail("copy: index space exceeds 2^31");
-    c.vec_per_row = static_cast<uint32_t>(g.n[0] / v);
-    if (static_cast<uint64_t>(c.vec_per_row) * c.rows.total >= kIdxLimit)
+    if (!build_space(g, xs, &c.X) || !build_space(g, ys, &c.Y) ||
+        !build_space(g, outer_axes(g, xs, ys, 0), &c.O))
       return fail("copy: index space exceeds 2^31");
-    c.vpr = Div32::make(c.vec_per_row);
-    c.total_vec = c.vec_per_row * c.rows.total;
-    const int occ = std::min(occ_cap, std::max(1, occupancy_copy(g.ka, g.kb, v, g.mode, 256)));
-    const int64_t want = (static_cast<int64_t>(c.total_vec) + 256 * 4 - 1) / (256 * 4);
+    c.lvec = static_cast<uint32_t>(g.n[0] / v);
+    c.dl = Div32::make(c.lvec);
+    c.tx = static_cast<uint32_t>(tx);
+    c.ty = static_cast<uint32_t>(ty);
+    c.ltx = c.lty = 0;
+    while ((1u << c.ltx) < c.tx) ++c.ltx;
+    while ((1u << c.lty) < c.ty) ++c.lty;
+    c.nxc = (c.X.total + c.tx - 1) / c.tx;
+    c.nyc = (c.Y.total + c.ty - 1) / c.ty;
+    c.dnx = Div32::make(c.nxc);
+    c.dny = Div32::make(c.nyc);
+    c.order = s.order;
+    const uint64_t rows = uint64_t{c.nxc} * c.nyc * c.O.total * c.tx * c.ty;  // incl. masked
+    constexpr uint32_t kSeg = 32 * 8;  // vectors per warp item (copy_rows_kernel U = 8)
+    c.long_rows = c.lvec >= 128 ? 1 : 0;
+    c.nseg = (c.lvec + kSeg - 1) / kSeg;
+    c.dseg = Div32::make(c.nseg);
+    const uint64_t items = c.long_rows ? rows * c.nseg : rows * c.lvec;
+    if (rows >= kIdxLimit || items >= kIdxLimit) return fail("copy: index space exceeds 2^31");
+    c.items = static_cast<uint32_t>(items);
+    const int occ = std::min(
+        occ_cap, std::max(1, occupancy_copy(g.ka, g.kb, v, g.mode, c.long_rows != 0, 256)));
+    const int64_t want = c.long_rows ? (static_cast<int64_t>(c.items) + 7) / 8
+                                     : (static_cast<int64_t>(c.items) + 256 * 4 - 1) / (256 * 4);
     p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t{occ} * sms)));
     p.a_align = v * g.eA;
     p.b_align = v * g.eB;
@@ -445,6 +526,8 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
         !build_space(g, outer_axes(g, xs, ys, -1), &r.O))
       return fail("rt: index space exceeds 2^31");
     r.lx = s.lx;
+    r.lx_log2 = 0;
+    while ((1 << r.lx_log2) < s.lx) ++r.lx_log2;
     r.wx = static_cast<uint32_t>(s.lx * mx);
     r.wy = static_cast<uint32_t>((32 / s.lx) * my);
     r.nxc = (r.X.total + r.wx - 1) / r.wx;
@@ -475,9 +558,19 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
         !build_space(g, outer_axes(g, xs, ys, shared ? 0 : -1), &m.O))
       return fail("smem: index space exceeds 2^31");
     m.S = shared ? static_cast<uint32_t>(g.n[0]) : 1;
-    if (s.tx < 1 || s.ty < 1) return fail("smem: empty tile");
-    m.tx = static_cast<uint32_t>(std::min<int64_t>(s.tx, m.X.total));
-    m.ty = static_cast<uint32_t>(std::min<int64_t>(s.ty, m.Y.total));
+    if (s.tx < 1 || s.ty < 1 || s.tx > 4096 || s.ty > 4096) return fail("smem: bad tile");
+    const bool pow2 = (s.tx & (s.tx - 1)) == 0 && (s.ty & (s.ty - 1)) == 0;
+    m.dense = !shared && pow2 && x_dense_in_a(g, xs) && y_dense_in_b(g, ys);
+    if (m.dense) {  // masked power-of-two tile (partial tiles at the group ends)
+      m.tx = static_cast<uint32_t>(s.tx);
+      m.ty = static_cast<uint32_t>(s.ty);
+      m.ltx = m.lty = 0;
+      while ((1u << m.ltx) < m.tx) ++m.ltx;
+      while ((1u << m.lty) < m.ty) ++m.lty;
+    } else {
+      m.tx = static_cast<uint32_t>(std::min<int64_t>(s.tx, m.X.total));
+      m.ty = static_cast<uint32_t>(std::min<int64_t>(s.ty, m.Y.total));
+    }
     m.rl = best_row_length(m.S, m.tx, m.ty, g.eA);
     m.dS = Div32::make(m.S);
     m.dtx = Div32::make(m.tx);
@@ -494,7 +587,8 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
                          static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);
-    const int occ = std::min(occ_cap, std::max(1, occupancy_smem(g.ka, g.kb, g.mode, 256, p.l.smem)));
+    const int occ = std::min(
+        occ_cap, std::max(1, occupancy_smem(g.ka, g.kb, g.mode, m.dense != 0, 256, p.l.smem)));
     p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(m.items, int64_t{occ} * sms)));
     p.a_align = std::min(16, g.eA);  // whole elements (Vec<SA, C>) move as a unit
     p.b_align = std::min(16, g.eB);

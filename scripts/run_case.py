@@ -1,0 +1,73 @@
+#!/usr/bin/env python3
+"""Time one BASELINE workload (config or c5 row) under every candidate plan, or
+under one given plan -- the driver for kernel tuning and ncu captures.
+
+    python scripts/run_case.py c5_t00 [--plan TEXT] [--iters 20] [--check]
+
+Prints one line per plan: device time (CUDA events, best of iters) and GB/s
+(tuner.cpp:18-25 byte count).  --check compares the output checksum with the
+reference's golden checksum (tests/golden/config_checksums.json).
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("case")
+    ap.add_argument("--plan", default=None)
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--check", action="store_true")
+    ap.add_argument("--top", type=int, default=0, help="only the first N candidates")
+    args = ap.parse_args()
+
+    import torch
+    import paper_1603_02297_b200 as ttb
+    from paper_1603_02297_b200.workloads import BY_NAME
+
+    w = BY_NAME[args.case]
+    p = ttb.make_problem(w.perm, list(w.sizes), w.kind, w.kind, w.alpha, w.beta,
+                         w.lda and list(w.lda), w.ldb and list(w.ldb))
+    na, nb = ttb.required_elements_a(p), ttb.required_elements_b(p)
+    a, b = ttb.TensorBuffer(w.kind, na), ttb.TensorBuffer(w.kind, nb)
+    ttb.fill_sentinel(w.kind, na, a.data_ptr())
+    ttb.fill_uniform(w.kind, list(w.sizes), w.lda and list(w.lda), w.seed_a, a.data_ptr())
+    plan = ttb.GpuPlan(p, cache=False)
+    texts = [args.plan] if args.plan else plan.candidates()
+    if args.top:
+        texts = texts[:args.top]
+    golden = None
+    if args.check:
+        with open(os.path.join(ROOT, "tests", "golden", "config_checksums.json")) as f:
+            golden = int(json.load(f)[w.name]["checksum"])
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    merged = ttb.merge_indices(p).problem
+    print(f"# {w.name} kind={w.kind} merged perm={merged.perm.map} sizes={merged.sizes} "
+          f"bytes={w.algorithmic_bytes}", flush=True)
+    for t in texts:
+        plan.select(t)
+        if w.beta != 0.0:
+            ttb.fill_uniform(w.kind, w.sizes_b, w.ldb and list(w.ldb), w.seed_b, b.data_ptr())
+        plan.execute(a, b)
+        ok = ""
+        if golden is not None:
+            ck = ttb.checksum(w.kind, w.sizes_b, w.ldb and list(w.ldb), b.data_ptr())
+            ok = " ok" if ck == golden else " MISMATCH"
+        best = 1e30
+        for _ in range(args.iters):
+            e0.record()
+            plan.execute(a, b)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        print(f"{best * 1e3:9.1f} us {w.algorithmic_bytes / 1e9 / (best / 1e3):8.1f} GB/s  {t}{ok}",
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()

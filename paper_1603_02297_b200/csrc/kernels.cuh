@@ -504,75 +504,130 @@ __global__ void __launch_bounds__(256) smem_kernel(const SmemParams P) {
 
 namespace ttb {
 
+// asynchronous global -> shared copy of one element (LDGSTS): no register
+// staging, so a thread can keep its whole share of a tile in flight
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem_dst, const void* gsrc) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(s), "l"(gsrc), "n"(BYTES)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+struct DenseTile {
+  uint32_t x0, y0, nx, ny, o;
+};
+
+__device__ __forceinline__ DenseTile dense_tile(const SmemParams& P, uint32_t it) {
+  DenseTile t;
+  uint32_t xc, yc;
+  if (P.order == 0) {
+    const uint32_t q = udiv(it, P.dnx);
+    xc = it - q * P.nxc;
+    t.o = udiv(q, P.dny);
+    yc = q - t.o * P.nyc;
+  } else {
+    const uint32_t q = udiv(it, P.dny);
+    yc = it - q * P.nyc;
+    t.o = udiv(q, P.dnx);
+    xc = q - t.o * P.nxc;
+  }
+  t.x0 = xc * P.tx;
+  t.y0 = yc * P.ty;
+  t.nx = min(P.tx, P.X.total - t.x0);
+  t.ny = min(P.ty, P.Y.total - t.y0);
+  return t;
+}
+
 // Dense fast path of the staged tile (the common case after index merging):
 // no shared stride-1 index, the X group is one contiguous run of A and the Y
-// group one contiguous run of B, tile extents are powers of two.  Per tile the
-// A offset of every row (y) and the B offset of every column (x) go to shared
-// memory; each element then costs a mask, a shift and one warp-broadcast
-// table read on either walk -- no division.
+// group one contiguous run of B.  Per tile the A offset of every row (y) and
+// the B offset of every column (x) go to shared memory, so an element costs a
+// split of its tile position and one warp-broadcast table read on either
+// walk.  Two tile buffers: the cp.async loads of the next tile are in flight
+// while the current tile is written out.
 template <class SA, class SB, int C, int MODE>
 __global__ void __launch_bounds__(256) smem_dense_kernel(const SmemParams P) {
   using E = Vec<SA, C>;
+  constexpr int EB = static_cast<int>(sizeof(E));
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int64_t* rowA = reinterpret_cast<int64_t*>(smem_raw);  // [ty]: A offset of (x0, y0 + y)
-  int64_t* colB = rowA + P.ty;                            // [tx]: B offset of (x0 + x, y0)
-  E* tile = reinterpret_cast<E*>(colB + P.tx);
+  const uint32_t table_bytes = ((P.tx + P.ty) * 8 + 15) & ~15u;
+  const uint32_t stage_bytes = table_bytes + ((P.ty * P.rl * EB + 15) & ~15u);
+  auto rowA = [&](int s) { return reinterpret_cast<int64_t*>(smem_raw + s * stage_bytes); };
+  auto colB = [&](int s) { return rowA(s) + P.ty; };
+  auto tile = [&](int s) { return reinterpret_cast<E*>(smem_raw + s * stage_bytes + table_bytes); };
 
   const Update<SA, SB, MODE> up(P.sc);
   const SA* __restrict__ A = static_cast<const SA*>(P.A);
   SB* __restrict__ B = static_cast<SB*>(P.B);
   const uint32_t L = P.tx * P.ty;
-  const uint32_t mx = P.tx - 1, my = P.ty - 1;
 
-  for (uint32_t it = blockIdx.x; it < P.items; it += gridDim.x) {
-    uint32_t xc, yc, o;
-    if (P.order == 0) {
-      const uint32_t t = udiv(it, P.dnx);
-      xc = it - t * P.nxc;
-      o = udiv(t, P.dny);
-      yc = t - o * P.nyc;
-    } else {
-      const uint32_t t = udiv(it, P.dny);
-      yc = it - t * P.nyc;
-      o = udiv(t, P.dnx);
-      xc = t - o * P.nxc;
-    }
-    const uint32_t x0 = xc * P.tx, y0 = yc * P.ty;
-    const uint32_t nx = min(P.tx, P.X.total - x0), ny = min(P.ty, P.Y.total - y0);
+  auto tables = [&](const DenseTile& t, int s) {
     int64_t aO, bO;
-    decode(P.O, o, aO, bO);
-    for (uint32_t i = threadIdx.x; i < ny; i += blockDim.x) {
+    decode(P.O, t.o, aO, bO);
+    int64_t* ra = rowA(s);
+    int64_t* cb = colB(s);
+    for (uint32_t i = threadIdx.x; i < t.ny; i += blockDim.x) {
       int64_t a, b;
-      decode(P.Y, y0 + i, a, b);
-      rowA[i] = a + aO + x0;
+      decode(P.Y, t.y0 + i, a, b);
+      ra[i] = a + aO + t.x0;
     }
-    for (uint32_t i = threadIdx.x; i < nx; i += blockDim.x) {
+    for (uint32_t i = threadIdx.x; i < t.nx; i += blockDim.x) {
       int64_t a, b;
-      decode(P.X, x0 + i, a, b);
-      colB[i] = b + bO + y0;
+      decode(P.X, t.x0 + i, a, b);
+      cb[i] = b + bO + t.y0;
     }
-    __syncthreads();
-
-    constexpr int U = 8;
-    for (uint32_t f0 = threadIdx.x; f0 < L; f0 += U * blockDim.x) {
-      E v[U];
-      int dst[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t f = f0 + u * blockDim.x;
-        const uint32_t x = f & mx, y = f >> P.ltx;
-        dst[u] = -1;
-        if (f < L && x < nx && y < ny) {
-          vload_a(v[u], A + (rowA[y] + x) * C);
-          dst[u] = static_cast<int>(y * P.rl + x);
-        }
+  };
+  // A -> smem: A-contiguous walk (x fastest), all of it asynchronous
+  auto loads = [&](const DenseTile& t, int s) {
+    const int64_t* ra = rowA(s);
+    E* tl = tile(s);
+    for (uint32_t f = threadIdx.x; f < L; f += blockDim.x) {
+      uint32_t x, y;
+      if (P.dense == 2) {
+        x = f & (P.tx - 1);
+        y = f >> P.ltx;
+      } else {
+        y = udiv(f, P.dtx);
+        x = f - y * P.tx;
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (dst[u] >= 0) tile[dst[u]] = v[u];
+      if (x < t.nx && y < t.ny) cp_async<EB>(tl + y * P.rl + x, A + (ra[y] + x) * C);
+    }
+  };
+
+  uint32_t it = blockIdx.x;
+  if (it >= P.items) return;
+  DenseTile cur = dense_tile(P, it);
+  tables(cur, 0);
+  __syncthreads();
+  loads(cur, 0);
+  cp_async_commit();
+  for (int s = 0; it < P.items; it += gridDim.x, s ^= 1) {
+    const uint32_t nxt = it + gridDim.x;
+    DenseTile nt{};
+    if (nxt < P.items) {
+      nt = dense_tile(P, nxt);
+      tables(nt, s ^ 1);
     }
     __syncthreads();
+    if (nxt < P.items) loads(nt, s ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();  // this thread's copies of the current tile have landed
+    __syncthreads();     // ... and everyone else's
 
+    // smem -> B: B-contiguous walk (y fastest)
+    const int64_t* cb = colB(s);
+    const E* tl = tile(s);
+    constexpr int U = 8;
     for (uint32_t f0 = threadIdx.x; f0 < L; f0 += U * blockDim.x) {
       Vec<SB, C> w[U];
       E a[U];
@@ -580,12 +635,19 @@ __global__ void __launch_bounds__(256) smem_dense_kernel(const SmemParams P) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t f = f0 + u * blockDim.x;
-        const uint32_t y = f & my, x = f >> P.lty;
+        uint32_t x, y;
+        if (P.dense == 2) {
+          y = f & (P.ty - 1);
+          x = f >> P.lty;
+        } else {
+          x = udiv(f, P.dty);
+          y = f - x * P.ty;
+        }
         q[u] = nullptr;
-        if (f < L && x < nx && y < ny) {
-          q[u] = B + (colB[x] + y) * C;
+        if (f < L && x < cur.nx && y < cur.ny) {
+          q[u] = B + (cb[x] + y) * C;
           if constexpr (MODE == 2) vload_b(w[u], q[u]);
-          a[u] = tile[y * P.rl + x];
+          a[u] = tl[y * P.rl + x];
         }
       }
 #pragma unroll
@@ -597,6 +659,7 @@ __global__ void __launch_bounds__(256) smem_dense_kernel(const SmemParams P) {
       }
     }
     __syncthreads();
+    cur = nt;
   }
 }
 

@@ -200,9 +200,15 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
       if (NX >= int64_t{1} << 31 || NY >= int64_t{1} << 31) break;
       const bool dense = !shared && x_dense_in_a(g, xs) && y_dense_in_b(g, ys);
       std::vector<int64_t> txs, tys;
-      if (dense) {  // powers of two, capped at the group extent rounded up
-        for (int64_t t = 1; t <= std::min<int64_t>(1024, pow2_ceil(NX)); t *= 2) txs.push_back(t);
-        for (int64_t t = 1; t <= std::min<int64_t>(1024, pow2_ceil(NY)); t *= 2) tys.push_back(t);
+      if (dense) {  // powers of two (masked ends) and exact divisors of the extents
+        auto sides = [](int64_t N, std::vector<int64_t>* v) {
+          for (int64_t t = 1; t <= std::min<int64_t>(1024, pow2_ceil(N)); t *= 2) v->push_back(t);
+          for (int64_t k = 1; k <= 64; ++k)
+            if (N % k == 0 && N / k >= 8 && N / k <= 1024 && (N / k & (N / k - 1)))
+              v->push_back(N / k);
+        };
+        sides(NX, &txs);
+        sides(NY, &tys);
       } else {
         for (int64_t t : {8, 16, 32, 64, 128, 256})
           if (t < NX) txs.push_back(t);
@@ -214,21 +220,31 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
       for (int64_t tx : txs) {
         for (int64_t ty : tys) {
           const int64_t bytes = S * tx * ty * g.eA;
-          if (bytes < 4096 && !(tx >= NX && ty >= NY)) continue;
-          if (bytes > 40 * 1024) continue;
+          // the dense kernel double-buffers: ~8 KB tiles keep ~6 CTAs per SM
+          const int64_t ideal = dense ? 8192 : 16384, cap = dense ? 20 * 1024 : 40 * 1024;
+          if (bytes < 2048 && !(tx >= NX && ty >= NY)) continue;
+          if (bytes > cap) continue;
           const double ex = static_cast<double>(NX) / (((NX + tx - 1) / tx) * tx);
           const double ey = static_cast<double>(NY) / (((NY + ty - 1) / ty) * ty);
-          const int64_t run_a = S * std::min(tx, NX) * g.eA, run_b = S * std::min(ty, NY) * g.eB;
+          // contiguous bytes per tile row in A / per tile column in B; a side
+          // that covers its whole group continues into the other group when
+          // that group's first axis is the next one in memory
+          int64_t run_a = S * std::min(tx, NX) * g.eA, run_b = S * std::min(ty, NY) * g.eB;
+          if (tx >= NX && g.sa[ys[0]] == S * NX) run_a *= std::min<int64_t>(ty, g.n[ys[0]]);
+          if (ty >= NY && g.sb[xs[0]] == S * NY) run_b *= std::min<int64_t>(tx, g.n[xs[0]]);
+          auto run_cost = [](int64_t r) {
+            return r < 32 ? 8.0 : r < 64 ? 4.0 : r < 128 ? 2.0 : r < 256 ? 0.7 : 0.0;
+          };
           Spec s;
           s.v = kSmem;
           s.kx = kx;
           s.ky = ky;
           s.tx = static_cast<int>(tx);
           s.ty = static_cast<int>(ty);
-          s.cost = 2.0 + (1.0 - ex * ey) * 12.0 + (run_a < 256 ? (run_a < 128 ? 2.0 : 1.0) : 0.0) +
-                   (run_b < 256 ? (run_b < 128 ? 2.0 : 1.0) : 0.0) +
-                   std::fabs(std::log2(static_cast<double>(bytes) / 16384.0)) * 0.3 +
-                   (dense ? 0.0 : 1.0) + 0.05 * (kx + ky);
+          s.cost = 2.0 + (1.0 - ex * ey) * 12.0 + run_cost(run_a) + run_cost(run_b) +
+                   std::fabs(std::log2(static_cast<double>(bytes) / ideal)) * 0.3 +
+                   (dense ? 0.0 : 1.0) + 0.05 * (kx + ky) +
+                   ((tx & (tx - 1)) || (ty & (ty - 1)) ? 0.2 : 0.0);
           cand.push_back(s);
         }
       }
@@ -357,6 +373,14 @@ std::vector<Spec> candidates(const Geo& g) {
     const int64_t nx = g.r > 1 ? g.n[1] : 1, ny = ky ? g.n[g.at[1]] : 1;
     const int64_t row_bytes = g.n[0] * emax;
     for (int w = v; w >= 1; w /= 2) {
+      // rows in plain B order: B written sequentially, A read row by row
+      Spec b;
+      b.v = kCopy;
+      b.w1 = w;
+      b.kx = b.ky = 0;
+      b.tx = b.ty = 1;
+      b.cost = cost + (v / w) * 0.5 - 0.1;
+      out.push_back(b);
       for (auto t : {std::pair<int, int>{1, 1}, {8, 8}, {4, 16}, {16, 4}, {32, 1}, {2, 2}}) {
         const int tx = static_cast<int>(std::min<int64_t>(t.first, pow2_ceil(nx)));
         const int ty = ky ? static_cast<int>(std::min<int64_t>(t.second, pow2_ceil(ny))) : 1;
@@ -468,7 +492,7 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     for (int a = 1; a < g.r; ++a)
       if (g.sa[a] % v || g.sb[a] % v) return fail("copy: strides not vector aligned");
     if (s.kx < 0 || s.ky < 0 || s.kx > 1 || s.ky > 1) return fail("copy: bad row groups");
-    if (s.kx == 0 && g.r > 1) return fail("copy: rows need the X group");
+    if (s.kx == 0 && s.ky == 1) return fail("copy: Y group needs an X group");
     const std::vector<int> xs = s.kx ? std::vector<int>{1} : std::vector<int>{};
     const std::vector<int> ys = s.ky ? std::vector<int>{g.at[1]} : std::vector<int>{};
     if (s.ky && !disjoint(xs, ys)) return fail("copy: X/Y groups overlap");
@@ -560,8 +584,9 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     m.S = shared ? static_cast<uint32_t>(g.n[0]) : 1;
     if (s.tx < 1 || s.ty < 1 || s.tx > 4096 || s.ty > 4096) return fail("smem: bad tile");
     const bool pow2 = (s.tx & (s.tx - 1)) == 0 && (s.ty & (s.ty - 1)) == 0;
-    m.dense = !shared && pow2 && x_dense_in_a(g, xs) && y_dense_in_b(g, ys);
-    if (m.dense) {  // masked power-of-two tile (partial tiles at the group ends)
+    const bool dense = !shared && x_dense_in_a(g, xs) && y_dense_in_b(g, ys);
+    m.dense = dense ? (pow2 ? 2 : 1) : 0;
+    if (dense && pow2) {  // masked power-of-two tile (partial tiles at the group ends)
       m.tx = static_cast<uint32_t>(s.tx);
       m.ty = static_cast<uint32_t>(s.ty);
       m.ltx = m.lty = 0;
@@ -583,8 +608,11 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     const uint64_t items = uint64_t{m.nxc} * m.nyc * m.O.total;
     if (items >= kIdxLimit) return fail("smem: too many tiles");
     m.items = static_cast<uint32_t>(items);
-    const int64_t smem = static_cast<int64_t>(m.tx + m.ty) * 2 * 8 +
-                         static_cast<int64_t>(m.ty) * m.rl * g.eA;
+    const auto r16 = [](int64_t v) { return (v + 15) & ~int64_t{15}; };
+    const int64_t smem =
+        m.dense ? 2 * (r16(static_cast<int64_t>(m.tx + m.ty) * 8) +
+                       r16(static_cast<int64_t>(m.ty) * m.rl * g.eA))  // double-buffered
+                : static_cast<int64_t>(m.tx + m.ty) * 2 * 8 + static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);
     const int occ = std::min(

@@ -515,6 +515,72 @@ __device__ __forceinline__ void cp_async(void* smem_dst, const void* gsrc) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(s), "l"(gsrc), "n"(BYTES)
                  : "memory");
 }
+// predicated forms: nothing is touched when pred == 0 (masked tile edges)
+template <int BYTES>
+__device__ __forceinline__ void cp_async_pred(void* smem_dst, const void* gsrc, bool pred) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  if constexpr (BYTES == 16)
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %2, 0; @p cp.async.cg.shared.global [%0], [%1], 16; }" ::"r"(s),
+        "l"(gsrc), "r"(static_cast<int>(pred))
+        : "memory");
+  else
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %2, 0; @p cp.async.ca.shared.global [%0], [%1], %3; }" ::"r"(s),
+        "l"(gsrc), "r"(static_cast<int>(pred)), "n"(BYTES)
+        : "memory");
+}
+
+template <class T, int N>
+__device__ __forceinline__ void vstore_pred(T* p, const Vec<T, N>& v, bool pred) {
+  constexpr int BYTES = sizeof(T) * N;
+  static_assert(BYTES == 4 || BYTES == 8 || BYTES == 16, "element store");
+  const int pr = static_cast<int>(pred);
+  if constexpr (BYTES == 16) {
+    const uint4 r = *reinterpret_cast<const uint4*>(v.v);
+    asm volatile("{ .reg .pred p; setp.ne.b32 p, %5, 0; @p st.global.v4.u32 [%0], {%1,%2,%3,%4}; }" ::"l"(p),
+                 "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w), "r"(pr)
+                 : "memory");
+  } else if constexpr (BYTES == 8) {
+    const uint2 r = *reinterpret_cast<const uint2*>(v.v);
+    asm volatile("{ .reg .pred p; setp.ne.b32 p, %3, 0; @p st.global.v2.u32 [%0], {%1,%2}; }" ::"l"(p),
+                 "r"(r.x), "r"(r.y), "r"(pr)
+                 : "memory");
+  } else {
+    const uint32_t r = *reinterpret_cast<const uint32_t*>(v.v);
+    asm volatile("{ .reg .pred p; setp.ne.b32 p, %2, 0; @p st.global.u32 [%0], %1; }" ::"l"(p), "r"(r),
+                 "r"(pr)
+                 : "memory");
+  }
+}
+
+template <class T, int N>
+__device__ __forceinline__ void vload_b_pred(Vec<T, N>& v, const T* p, bool pred) {
+  constexpr int BYTES = sizeof(T) * N;
+  static_assert(BYTES == 4 || BYTES == 8 || BYTES == 16, "element load");
+  const int pr = static_cast<int>(pred);
+  if constexpr (BYTES == 16) {
+    uint4 r = make_uint4(0, 0, 0, 0);
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %5, 0; @p ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4]; }"
+        : "+r"(r.x), "+r"(r.y), "+r"(r.z), "+r"(r.w)
+        : "l"(p), "r"(pr));
+    *reinterpret_cast<uint4*>(v.v) = r;
+  } else if constexpr (BYTES == 8) {
+    uint2 r = make_uint2(0, 0);
+    asm volatile("{ .reg .pred p; setp.ne.b32 p, %3, 0; @p ld.global.L1::no_allocate.v2.u32 {%0,%1}, [%2]; }"
+                 : "+r"(r.x), "+r"(r.y)
+                 : "l"(p), "r"(pr));
+    *reinterpret_cast<uint2*>(v.v) = r;
+  } else {
+    uint32_t r = 0;
+    asm volatile("{ .reg .pred p; setp.ne.b32 p, %2, 0; @p ld.global.L1::no_allocate.u32 %0, [%1]; }"
+                 : "+r"(r)
+                 : "l"(p), "r"(pr));
+    *reinterpret_cast<uint32_t*>(v.v) = r;
+  }
+}
+
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -555,14 +621,24 @@ __device__ __forceinline__ DenseTile dense_tile(const SmemParams& P, uint32_t it
 // split of its tile position and one warp-broadcast table read on either
 // walk.  Two tile buffers: the cp.async loads of the next tile are in flight
 // while the current tile is written out.
-template <class SA, class SB, int C, int MODE>
-__global__ void __launch_bounds__(256) smem_dense_kernel(const SmemParams P) {
+//
+// EPT > 0: tx, ty <= 256 are powers of two and tx*ty = 256*EPT, so a thread's
+// column (load walk) and row (store walk) are fixed for the whole kernel and
+// its EPT elements per walk sit at constant strides: each element costs one
+// table read, one address add and one predicated LDGSTS / STG.
+// EPT == 0: any tile shape, positions split per element.
+template <class SA, class SB, int C, int MODE, int EPT>
+__global__ void __launch_bounds__(256, (EPT > 0 && MODE < 2 && C == 1 && sizeof(SA) == sizeof(SB))
+                                           ? 6
+                                           : 4) smem_dense_kernel(const SmemParams P) {
   using E = Vec<SA, C>;
   constexpr int EB = static_cast<int>(sizeof(E));
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const uint32_t table_bytes = ((P.tx + P.ty) * 8 + 15) & ~15u;
+  // offsets are 32-bit: the planner only picks this kernel for tensors whose
+  // footprints stay below 2^31 elements
+  const uint32_t table_bytes = ((P.tx + P.ty) * 4 + 15) & ~15u;
   const uint32_t stage_bytes = table_bytes + ((P.ty * P.rl * EB + 15) & ~15u);
-  auto rowA = [&](int s) { return reinterpret_cast<int64_t*>(smem_raw + s * stage_bytes); };
+  auto rowA = [&](int s) { return reinterpret_cast<uint32_t*>(smem_raw + s * stage_bytes); };
   auto colB = [&](int s) { return rowA(s) + P.ty; };
   auto tile = [&](int s) { return reinterpret_cast<E*>(smem_raw + s * stage_bytes + table_bytes); };
 
@@ -574,23 +650,36 @@ __global__ void __launch_bounds__(256) smem_dense_kernel(const SmemParams P) {
   auto tables = [&](const DenseTile& t, int s) {
     int64_t aO, bO;
     decode(P.O, t.o, aO, bO);
-    int64_t* ra = rowA(s);
-    int64_t* cb = colB(s);
+    uint32_t* ra = rowA(s);
+    uint32_t* cb = colB(s);
     for (uint32_t i = threadIdx.x; i < t.ny; i += blockDim.x) {
       int64_t a, b;
       decode(P.Y, t.y0 + i, a, b);
-      ra[i] = a + aO + t.x0;
+      ra[i] = static_cast<uint32_t>(a + aO + t.x0);
     }
     for (uint32_t i = threadIdx.x; i < t.nx; i += blockDim.x) {
       int64_t a, b;
       decode(P.X, t.x0 + i, a, b);
-      cb[i] = b + bO + t.y0;
+      cb[i] = static_cast<uint32_t>(b + bO + t.y0);
     }
   };
   // A -> smem: A-contiguous walk (x fastest), all of it asynchronous
   auto loads = [&](const DenseTile& t, int s) {
-    const int64_t* ra = rowA(s);
+    const uint32_t* ra = rowA(s);
     E* tl = tile(s);
+    if constexpr (EPT > 0) {
+      const uint32_t xt = threadIdx.x & (P.tx - 1), yt = threadIdx.x >> P.ltx;
+      const uint32_t R = 256u >> P.ltx;
+      const bool xv = xt < t.nx;
+      const E* ax = reinterpret_cast<const E*>(A) + xt;
+      E* tx0 = tl + yt * P.rl + xt;
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const uint32_t y = yt + k * R;  // < ty: the table read is in bounds even when masked
+        cp_async_pred<EB>(tx0 + k * R * P.rl, ax + ra[y], xv && y < t.ny);
+      }
+      return;
+    }
     for (uint32_t f = threadIdx.x; f < L; f += blockDim.x) {
       uint32_t x, y;
       if (P.dense == 2) {
@@ -625,9 +714,41 @@ __global__ void __launch_bounds__(256) smem_dense_kernel(const SmemParams P) {
     __syncthreads();     // ... and everyone else's
 
     // smem -> B: B-contiguous walk (y fastest)
-    const int64_t* cb = colB(s);
+    const uint32_t* cb = colB(s);
     const E* tl = tile(s);
     constexpr int U = 8;
+    if constexpr (EPT > 0) {
+      const uint32_t yt = threadIdx.x & (P.ty - 1), xt = threadIdx.x >> P.lty;
+      const uint32_t Q = 256u >> P.lty;
+      const bool yv = yt < cur.ny;
+      using EBv = Vec<SB, C>;
+      EBv* by = reinterpret_cast<EBv*>(B) + yt;
+      const E* ty0 = tl + yt * P.rl + xt;
+#pragma unroll
+      for (int k0 = 0; k0 < EPT; k0 += U) {
+        EBv w[U];
+        E a[U];
+        EBv* q[U];
+        bool v[U];
+#pragma unroll
+        for (int u = 0; u < U && k0 + u < EPT; ++u) {
+          const uint32_t x = xt + (k0 + u) * Q;  // < tx: table read in bounds when masked
+          v[u] = yv && x < cur.nx;
+          q[u] = by + cb[x];
+          if constexpr (MODE == 2) vload_b_pred(w[u], q[u]->v, v[u]);
+          a[u] = ty0[(k0 + u) * Q];
+        }
+#pragma unroll
+        for (int u = 0; u < U && k0 + u < EPT; ++u) {
+#pragma unroll
+          for (int c = 0; c < C; ++c) w[u].v[c] = up(a[u].v[c], w[u].v[c]);
+          vstore_pred(q[u]->v, w[u], v[u]);
+        }
+      }
+      __syncthreads();
+      cur = nt;
+      continue;
+    }
     for (uint32_t f0 = threadIdx.x; f0 < L; f0 += U * blockDim.x) {
       Vec<SB, C> w[U];
       E a[U];

@@ -245,6 +245,11 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
                    std::fabs(std::log2(static_cast<double>(bytes) / ideal)) * 0.3 +
                    (dense ? 0.0 : 1.0) + 0.05 * (kx + ky) +
                    ((tx & (tx - 1)) || (ty & (ty - 1)) ? 0.2 : 0.0);
+          // fixed-walk dense tiles (smem_dense_kernel EPT > 0) are the cheapest to issue
+          const int64_t e = tx * ty / 256;
+          if (dense && !(tx & (tx - 1)) && !(ty & (ty - 1)) && tx <= 256 && ty <= 256 &&
+              tx * ty == 256 * e && (e == 4 || e == 8 || e == 16))
+            s.cost -= 0.6;
           cand.push_back(s);
         }
       }
@@ -277,6 +282,8 @@ Geo make_geo(const Problem& m) {
   g.beta = m.beta;
   g.mode = mode_of(m.alpha, m.beta);
   g.elements = m.elements();
+  g.foot_a = m.footprint_a();
+  g.foot_b = m.footprint_b();
   return g;
 }
 
@@ -584,7 +591,8 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     m.S = shared ? static_cast<uint32_t>(g.n[0]) : 1;
     if (s.tx < 1 || s.ty < 1 || s.tx > 4096 || s.ty > 4096) return fail("smem: bad tile");
     const bool pow2 = (s.tx & (s.tx - 1)) == 0 && (s.ty & (s.ty - 1)) == 0;
-    const bool dense = !shared && x_dense_in_a(g, xs) && y_dense_in_b(g, ys);
+    const bool small = g.foot_a * g.C < (int64_t{1} << 31) && g.foot_b * g.C < (int64_t{1} << 31);
+    const bool dense = small && !shared && x_dense_in_a(g, xs) && y_dense_in_b(g, ys);
     m.dense = dense ? (pow2 ? 2 : 1) : 0;
     if (dense && pow2) {  // masked power-of-two tile (partial tiles at the group ends)
       m.tx = static_cast<uint32_t>(s.tx);
@@ -615,8 +623,13 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
                 : static_cast<int64_t>(m.tx + m.ty) * 2 * 8 + static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);
-    const int occ = std::min(
-        occ_cap, std::max(1, occupancy_smem(g.ka, g.kb, g.mode, m.dense != 0, 256, p.l.smem)));
+    m.ept = 0;
+    if (m.dense == 2 && m.tx <= 256 && m.ty <= 256) {
+      const uint32_t e = m.tx * m.ty / 256;
+      if (m.tx * m.ty == 256 * e && (e == 4 || e == 8 || e == 16)) m.ept = static_cast<int>(e);
+    }
+    const int occ = std::min(occ_cap, std::max(1, occupancy_smem(g.ka, g.kb, g.mode, m.dense != 0,
+                                                                 m.ept, 256, p.l.smem)));
     p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(m.items, int64_t{occ} * sms)));
     p.a_align = std::min(16, g.eA);  // whole elements (Vec<SA, C>) move as a unit
     p.b_align = std::min(16, g.eB);

@@ -27,6 +27,7 @@ struct Geo {
   int mode = 0;            // 0 move, 1 scale, 2 update
   double alpha = 1.0, beta = 0.0;
   int64_t elements = 1;
+  int64_t foot_a = 1, foot_b = 1;  // required_elements of A and B
 };
 Geo make_geo(const Problem& merged);
 

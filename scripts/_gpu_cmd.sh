@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q --durations=5 > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_gpu.log
-for c in c1 c2a c2b c3 c4 c4s c5_t00 c5_t04 c5_t08 c5_t10 c5_t12 c5_t15 c5_t22; do timeout 120 python scripts/run_case.py $c --iters 5 --check; done > gpurun_out/cases.log 2>&1
+P1="kern=smem;kx=2;ky=2;tx=64;ty=64;order=1;occ=0"
+timeout 120 python scripts/run_case.py c5_t00 --plan "$P1" --iters 3 > gpurun_out/p1.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:smem -s 2 -c 1 -o gpurun_out/prof_smem3_t00 python scripts/run_case.py c5_t00 --plan "$P1" --iters 3 > gpurun_out/ncu1.log 2>&1

@@ -83,5 +83,28 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines: list) -> str:
+    """Experiment build: every source with extra -D flags into _lib/libttb_<name>.so
+    (load it with TTB_LIB_PATH; the product always uses libttb.so)."""
+    objdir = os.path.join(LIBDIR, f"obj_{name}")
+    os.makedirs(objdir, exist_ok=True)
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
+
+    def one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [_nvcc(), *_flags(), *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
+        subprocess.run(cmd, check=True, capture_output=True)
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(one, srcs))
+    out = os.path.join(LIBDIR, f"libttb_{name}.so")
+    subprocess.run([_nvcc(), *ARCH, "-shared", "-ccbin", _host_cxx(), "-o", out, *objs], check=True)
+    return out
+
+
 if __name__ == "__main__":
-    print(build(verbose="--verbose" in sys.argv))
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        print(build(verbose="--verbose" in sys.argv))

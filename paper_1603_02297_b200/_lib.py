@@ -9,7 +9,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libttb.so")
+LIB_PATH = os.environ.get("TTB_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libttb.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

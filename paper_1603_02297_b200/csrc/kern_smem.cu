@@ -1,4 +1,7 @@
-// kern_smem.cu -- instantiation and launch of smem_kernel (staged tiles).
+// kern_smem.cu -- instantiation and launch of the staged-tile kernels:
+// tile_kernel (32-bit tables, the common case) and smem_kernel (64-bit).
+#include <cstdlib>
+
 #include "dispatch.cuh"
 #include "kernels.cuh"
 #include "launch.hpp"
@@ -7,30 +10,32 @@ namespace ttb {
 
 namespace {
 template <class F>
-cudaError_t with_smem(int ka, int kb, int mode, bool dense, int ept, F&& f) {
+cudaError_t with_smem(int ka, int kb, int mode, bool fast, F&& f) {
   return with_types(ka, kb, [&](auto t) {
     using T = decltype(t);
     return with_mode(mode, [&](auto m) {
       constexpr int M = decltype(m)::value;
-      using SA = typename T::SA;
-      using SB = typename T::SB;
-      if (dense) {
-        switch (ept) {
-          case 4: return f(&smem_dense_kernel<SA, SB, T::C, M, 4>);
-          case 8: return f(&smem_dense_kernel<SA, SB, T::C, M, 8>);
-          case 16: return f(&smem_dense_kernel<SA, SB, T::C, M, 16>);
-          default: return f(&smem_dense_kernel<SA, SB, T::C, M, 0>);
-        }
-      }
-      return f(&smem_kernel<typename T::SA, typename T::SB, T::C, decltype(m)::value>);
+      if (fast) return f(&tile_kernel<typename T::SA, typename T::SB, T::C, M>);
+      return f(&smem_kernel<typename T::SA, typename T::SB, T::C, M>);
     });
   });
+}
+
+int carveout() {
+  // shared/L1 split of the unified array (percent shared).  Half leaves L1 room
+  // for the cp.async (.ca) line allocations; TTB_CARVEOUT overrides, < 0 keeps
+  // the driver default.
+  static const int c = [] {
+    const char* e = std::getenv("TTB_CARVEOUT");
+    return e ? std::atoi(e) : 50;
+  }();
+  return c;
 }
 }  // namespace
 
 cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                         cudaStream_t s) {
-  return with_smem(ka, kb, mode, p.dense != 0, p.ept, [&](auto fn) {
+  return with_smem(ka, kb, mode, p.dense != 0, [&](auto fn) {
     if (l.smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
       if (e != cudaSuccess) return e;
@@ -41,12 +46,11 @@ cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Lau
   });
 }
 
-int occupancy_smem(int ka, int kb, int mode, bool dense, int ept, int block, int smem) {
+int occupancy_smem(int ka, int kb, int mode, bool fast, int /*ept*/, int block, int smem) {
   int n = 0;
-  with_smem(ka, kb, mode, dense, ept, [&](auto fn) {
-    // staged tiles want the whole unified L1/shared array as shared memory
-    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
+  with_smem(ka, kb, mode, fast, [&](auto fn) {
+    if (carveout() >= 0)
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout());
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem);
   });

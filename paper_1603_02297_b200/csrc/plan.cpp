@@ -198,32 +198,38 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
       if (!disjoint(xs, ys)) break;
       const int64_t NX = prod(g, xs), NY = prod(g, ys);
       if (NX >= int64_t{1} << 31 || NY >= int64_t{1} << 31) break;
-      const bool dense = !shared && x_dense_in_a(g, xs) && y_dense_in_b(g, ys);
+      // tile_kernel (32-bit tables, S*tx and S*ty <= 256) unless the tensors
+      // are too large for it, then the 64-bit smem_kernel
+      const bool fast = g.foot_a < (int64_t{1} << 31) && g.foot_b < (int64_t{1} << 31);
+      const int64_t side_cap = fast ? 256 / S : 1024;
+      if (side_cap < 1) continue;
+      auto sides = [&](int64_t N, std::vector<int64_t>* v) {
+        for (int64_t t : {2, 4, 8, 16, 32, 64, 128, 256, 512, 1024})
+          if (t < N && t <= side_cap) v->push_back(t);
+        if (N <= side_cap) v->push_back(N);
+        for (int64_t k = 2; k <= 64; ++k)  // exact divisors: no partial tiles
+          if (N % k == 0 && N / k >= 8 && N / k <= side_cap) v->push_back(N / k);
+      };
       std::vector<int64_t> txs, tys;
-      if (dense) {  // powers of two (masked ends) and exact divisors of the extents
-        auto sides = [](int64_t N, std::vector<int64_t>* v) {
-          for (int64_t t = 1; t <= std::min<int64_t>(1024, pow2_ceil(N)); t *= 2) v->push_back(t);
-          for (int64_t k = 1; k <= 64; ++k)
-            if (N % k == 0 && N / k >= 8 && N / k <= 1024 && (N / k & (N / k - 1)))
-              v->push_back(N / k);
-        };
-        sides(NX, &txs);
-        sides(NY, &tys);
-      } else {
-        for (int64_t t : {8, 16, 32, 64, 128, 256})
-          if (t < NX) txs.push_back(t);
-        txs.push_back(std::min<int64_t>(NX, 1024));
-        for (int64_t t : {8, 16, 32, 64, 128, 256})
-          if (t < NY) tys.push_back(t);
-        tys.push_back(std::min<int64_t>(NY, 1024));
-      }
+      sides(NX, &txs);
+      sides(NY, &tys);
       for (int64_t tx : txs) {
         for (int64_t ty : tys) {
           const int64_t bytes = S * tx * ty * g.eA;
-          // the dense kernel double-buffers: ~8 KB tiles keep ~6 CTAs per SM
-          const int64_t ideal = dense ? 8192 : 16384, cap = dense ? 20 * 1024 : 40 * 1024;
+          // tile_kernel double-buffers: ~8 KB tiles keep several CTAs per SM
+          const int64_t ideal = fast ? 8192 : 16384, cap = fast ? 20 * 1024 : 40 * 1024;
           if (bytes < 2048 && !(tx >= NX && ty >= NY)) continue;
           if (bytes > cap) continue;
+          // idle threads of the fixed-position walks (256 threads per CTA)
+          double util = 1.0;
+          if (fast) {
+            const int64_t LR = S * tx, LC = S * ty, R = 256 / LR, Q = 256 / LC;
+            const double ul = static_cast<double>(R * LR) / 256.0 *
+                              static_cast<double>(ty) / (((ty + R - 1) / R) * R);
+            const double us = static_cast<double>(Q * LC) / 256.0 *
+                              static_cast<double>(tx) / (((tx + Q - 1) / Q) * Q);
+            util = 0.5 * (ul + us);
+          }
           const double ex = static_cast<double>(NX) / (((NX + tx - 1) / tx) * tx);
           const double ey = static_cast<double>(NY) / (((NY + ty - 1) / ty) * ty);
           // contiguous bytes per tile row in A / per tile column in B; a side
@@ -243,13 +249,7 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
           s.ty = static_cast<int>(ty);
           s.cost = 2.0 + (1.0 - ex * ey) * 12.0 + run_cost(run_a) + run_cost(run_b) +
                    std::fabs(std::log2(static_cast<double>(bytes) / ideal)) * 0.3 +
-                   (dense ? 0.0 : 1.0) + 0.05 * (kx + ky) +
-                   ((tx & (tx - 1)) || (ty & (ty - 1)) ? 0.2 : 0.0);
-          // fixed-walk dense tiles (smem_dense_kernel EPT > 0) are the cheapest to issue
-          const int64_t e = tx * ty / 256;
-          if (dense && !(tx & (tx - 1)) && !(ty & (ty - 1)) && tx <= 256 && ty <= 256 &&
-              tx * ty == 256 * e && (e == 4 || e == 8 || e == 16))
-            s.cost -= 0.6;
+                   (1.0 - util) * 6.0 + 0.05 * (kx + ky);
           cand.push_back(s);
         }
       }
@@ -590,20 +590,14 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
       return fail("smem: index space exceeds 2^31");
     m.S = shared ? static_cast<uint32_t>(g.n[0]) : 1;
     if (s.tx < 1 || s.ty < 1 || s.tx > 4096 || s.ty > 4096) return fail("smem: bad tile");
-    const bool pow2 = (s.tx & (s.tx - 1)) == 0 && (s.ty & (s.ty - 1)) == 0;
-    const bool small = g.foot_a * g.C < (int64_t{1} << 31) && g.foot_b * g.C < (int64_t{1} << 31);
-    const bool dense = small && !shared && x_dense_in_a(g, xs) && y_dense_in_b(g, ys);
-    m.dense = dense ? (pow2 ? 2 : 1) : 0;
-    if (dense && pow2) {  // masked power-of-two tile (partial tiles at the group ends)
-      m.tx = static_cast<uint32_t>(s.tx);
-      m.ty = static_cast<uint32_t>(s.ty);
-      m.ltx = m.lty = 0;
-      while ((1u << m.ltx) < m.tx) ++m.ltx;
-      while ((1u << m.lty) < m.ty) ++m.lty;
-    } else {
-      m.tx = static_cast<uint32_t>(std::min<int64_t>(s.tx, m.X.total));
-      m.ty = static_cast<uint32_t>(std::min<int64_t>(s.ty, m.Y.total));
-    }
+    m.tx = static_cast<uint32_t>(std::min<int64_t>(s.tx, m.X.total));
+    m.ty = static_cast<uint32_t>(std::min<int64_t>(s.ty, m.Y.total));
+    // tile_kernel: 32-bit offset tables and one tile row / column per thread
+    // position; otherwise the general 64-bit smem_kernel
+    const bool small = g.foot_a < (int64_t{1} << 31) && g.foot_b < (int64_t{1} << 31);
+    m.dense = small && m.S * m.tx <= 256 && m.S * m.ty <= 256 ? 1 : 0;
+    m.ltx = m.lty = 0;
+    m.ept = 0;
     m.rl = best_row_length(m.S, m.tx, m.ty, g.eA);
     m.dS = Div32::make(m.S);
     m.dtx = Div32::make(m.tx);
@@ -623,11 +617,6 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
                 : static_cast<int64_t>(m.tx + m.ty) * 2 * 8 + static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);
-    m.ept = 0;
-    if (m.dense == 2 && m.tx <= 256 && m.ty <= 256) {
-      const uint32_t e = m.tx * m.ty / 256;
-      if (m.tx * m.ty == 256 * e && (e == 4 || e == 8 || e == 16)) m.ept = static_cast<int>(e);
-    }
     const int occ = std::min(occ_cap, std::max(1, occupancy_smem(g.ka, g.kb, g.mode, m.dense != 0,
                                                                  m.ept, 256, p.l.smem)));
     p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(m.items, int64_t{occ} * sms)));

@@ -1,2 +1,6 @@
-P1="kern=smem;kx=2;ky=2;tx=64;ty=64;order=1;occ=0"
-timeout 120 python scripts/run_case.py c5_t00 --plan "$P1" --iters 3 > gpurun_out/p1.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:smem -s 2 -c 1 -o gpurun_out/prof_smem3_t00 python scripts/run_case.py c5_t00 --plan "$P1" --iters 3 > gpurun_out/ncu1.log 2>&1
+for lib in libttb.so libttb_mb1.so libttb_mb4.so; do
+for cv in -1 50; do
+for c in c5_t00 c5_t16 c5_t22; do
+  echo "== lib=$lib cv=$cv"
+  TTB_LIB_PATH=$PWD/paper_1603_02297_b200/_lib/$lib TTB_CARVEOUT=$cv timeout 200 python scripts/run_case.py $c --iters 5 --top 8
+done; done; done > gpurun_out/var.log 2>&1

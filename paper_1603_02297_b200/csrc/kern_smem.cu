@@ -10,13 +10,22 @@ namespace ttb {
 
 namespace {
 template <class F>
-cudaError_t with_smem(int ka, int kb, int mode, bool fast, F&& f) {
+cudaError_t with_smem(int ka, int kb, int mode, bool fast, int kk, F&& f) {
   return with_types(ka, kb, [&](auto t) {
     using T = decltype(t);
+    using SA = typename T::SA;
+    using SB = typename T::SB;
     return with_mode(mode, [&](auto m) {
       constexpr int M = decltype(m)::value;
-      if (fast) return f(&tile_kernel<typename T::SA, typename T::SB, T::C, M>);
-      return f(&smem_kernel<typename T::SA, typename T::SB, T::C, M>);
+      if (fast) {
+        switch (kk) {
+          case 4: return f(&tile_kernel<SA, SB, T::C, M, 4>);
+          case 8: return f(&tile_kernel<SA, SB, T::C, M, 8>);
+          case 16: return f(&tile_kernel<SA, SB, T::C, M, 16>);
+          default: return f(&tile_kernel<SA, SB, T::C, M, 0>);
+        }
+      }
+      return f(&smem_kernel<SA, SB, T::C, M>);
     });
   });
 }
@@ -35,7 +44,7 @@ int carveout() {
 
 cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                         cudaStream_t s) {
-  return with_smem(ka, kb, mode, p.dense != 0, [&](auto fn) {
+  return with_smem(ka, kb, mode, p.dense != 0, p.ept, [&](auto fn) {
     if (l.smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
       if (e != cudaSuccess) return e;
@@ -46,9 +55,9 @@ cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Lau
   });
 }
 
-int occupancy_smem(int ka, int kb, int mode, bool fast, int /*ept*/, int block, int smem) {
+int occupancy_smem(int ka, int kb, int mode, bool fast, int ept, int block, int smem) {
   int n = 0;
-  with_smem(ka, kb, mode, fast, [&](auto fn) {
+  with_smem(ka, kb, mode, fast, ept, [&](auto fn) {
     if (carveout() >= 0)
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout());
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -597,7 +597,13 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     const bool small = g.foot_a < (int64_t{1} << 31) && g.foot_b < (int64_t{1} << 31);
     m.dense = small && m.S * m.tx <= 256 && m.S * m.ty <= 256 ? 1 : 0;
     m.ltx = m.lty = 0;
-    m.ept = 0;
+    m.ept = 0;  // tile_kernel KK: both walks exactly KK steps long
+    if (m.dense) {
+      const uint32_t LR = m.S * m.tx, LC = m.S * m.ty, L = m.S * m.tx * m.ty;
+      const uint32_t kk = L / 256;
+      if (256 % LR == 0 && 256 % LC == 0 && L == 256 * kk && (kk == 4 || kk == 8 || kk == 16))
+        m.ept = static_cast<int>(kk);
+    }
     m.rl = best_row_length(m.S, m.tx, m.ty, g.eA);
     m.dS = Div32::make(m.S);
     m.dtx = Div32::make(m.tx);

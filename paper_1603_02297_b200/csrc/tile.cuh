@@ -44,7 +44,10 @@ __device__ __forceinline__ TileBox tile_box(const SmemParams& P, uint32_t it) {
   return t;
 }
 
-template <class SA, class SB, int C, int MODE>
+// KK > 0: both walks have exactly KK steps covering the tile (S*tx and S*ty
+// divide 256 and tx*ty*S = 256*KK), so the loops unroll completely and need
+// neither a step bound nor a table clamp.  KK == 0: any shape.
+template <class SA, class SB, int C, int MODE, int KK>
 __global__ void __launch_bounds__(256) tile_kernel(const SmemParams P) {
   using EA = Vec<SA, C>;
   using EBv = Vec<SB, C>;
@@ -69,7 +72,9 @@ __global__ void __launch_bounds__(256) tile_kernel(const SmemParams P) {
   const uint32_t s_l = i_l % P.S, x_l = i_l / P.S;
   const uint32_t j_s = tid % LC, c0 = tid / LC;
   const uint32_t s_s = j_s % P.S, y_s = j_s / P.S;
-  const uint32_t K1 = (P.ty + R - 1) / R, K2 = (P.tx + Q - 1) / Q;
+  const uint32_t K1 = KK > 0 ? KK : (P.ty + R - 1) / R;
+  const uint32_t K2 = KK > 0 ? KK : (P.tx + Q - 1) / Q;
+  constexpr uint32_t UN = KK > 0 ? KK : 4;  // unroll of the walks
 
   auto tables = [&](const TileBox& t, int s) {
     int64_t aO, bO;
@@ -95,13 +100,13 @@ __global__ void __launch_bounds__(256) tile_kernel(const SmemParams P) {
     const EA* a0 = A + (vx ? T[x_l] : 0u) + s_l;
     const uint32_t* offAY = T + 2 * P.tx;
     EA* dst = tile(s) + r0 * P.rl + i_l;
-    for (uint32_t k0 = 0; k0 < K1; k0 += 4) {
+    for (uint32_t k0 = 0; k0 < K1; k0 += UN) {
 #pragma unroll
-      for (uint32_t u = 0; u < 4; ++u) {
+      for (uint32_t u = 0; u < UN; ++u) {
         const uint32_t k = k0 + u;
         const uint32_t y = r0 + k * R;
-        const bool v = vx && k < K1 && y < t.ny;
-        cp_async_pred<EAB>(dst + k * R * P.rl, a0 + offAY[min(y, P.ty - 1)], v);
+        const bool v = vx && (KK > 0 || k < K1) && y < t.ny;
+        cp_async_pred<EAB>(dst + k * R * P.rl, a0 + offAY[KK > 0 ? y : min(y, P.ty - 1)], v);
       }
     }
   };
@@ -133,22 +138,24 @@ __global__ void __launch_bounds__(256) tile_kernel(const SmemParams P) {
       EBv* b0 = B + (vy ? T[2 * P.tx + P.ty + y_s] : 0u) + s_s;
       const uint32_t* offBX = T + P.tx;
       const EA* src = tile(s) + y_s * P.rl + s_s;
-      for (uint32_t k0 = 0; k0 < K2; k0 += 4) {
-        EBv w[4];
-        EA a[4];
-        EBv* q[4];
-        bool v[4];
+      constexpr uint32_t U2 = UN > 8 ? 8 : UN;  // B loads in flight per batch
+      for (uint32_t k0 = 0; k0 < K2; k0 += U2) {
+        EBv w[U2];
+        EA a[U2];
+        EBv* q[U2];
+        bool v[U2];
 #pragma unroll
-        for (uint32_t u = 0; u < 4; ++u) {
+        for (uint32_t u = 0; u < U2; ++u) {
           const uint32_t k = k0 + u;
           const uint32_t x = c0 + k * Q;
-          v[u] = vy && k < K2 && x < cur.nx;
-          q[u] = b0 + offBX[min(x, P.tx - 1)];
+          const uint32_t xc = KK > 0 ? x : min(x, P.tx - 1);
+          v[u] = vy && (KK > 0 || k < K2) && x < cur.nx;
+          q[u] = b0 + offBX[xc];
           if constexpr (MODE == 2) vload_b_pred(w[u], q[u]->v, v[u]);
-          a[u] = src[min(x, P.tx - 1) * P.S];
+          a[u] = src[xc * P.S];
         }
 #pragma unroll
-        for (uint32_t u = 0; u < 4; ++u) {
+        for (uint32_t u = 0; u < U2; ++u) {
 #pragma unroll
           for (int c = 0; c < C; ++c) w[u].v[c] = up(a[u].v[c], w[u].v[c]);
           vstore_pred(q[u]->v, w[u], v[u]);

@@ -1,6 +1,2 @@
-for lib in libttb.so libttb_mb1.so libttb_mb4.so; do
-for cv in -1 50; do
-for c in c5_t00 c5_t16 c5_t22; do
-  echo "== lib=$lib cv=$cv"
-  TTB_LIB_PATH=$PWD/paper_1603_02297_b200/_lib/$lib TTB_CARVEOUT=$cv timeout 200 python scripts/run_case.py $c --iters 5 --top 8
-done; done; done > gpurun_out/var.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_gpu.log
+for c in c4s c5_t00 c5_t02 c5_t06 c5_t08 c5_t10 c5_t12 c5_t14 c5_t16 c5_t18 c5_t20 c5_t22; do timeout 120 python scripts/run_case.py $c --iters 5 --check; done > gpurun_out/cases.log 2>&1

@@ -9,15 +9,24 @@
 namespace ttb {
 
 namespace {
+// dense: 2 -> dense_kernel (power-of-two fast path, kk = EPT), 1 -> tile_kernel
+// (kk = compile-time walk length or 0), 0 -> smem_kernel (64-bit offsets)
 template <class F>
-cudaError_t with_smem(int ka, int kb, int mode, bool fast, int kk, F&& f) {
+cudaError_t with_smem(int ka, int kb, int mode, int dense, int kk, F&& f) {
   return with_types(ka, kb, [&](auto t) {
     using T = decltype(t);
     using SA = typename T::SA;
     using SB = typename T::SB;
     return with_mode(mode, [&](auto m) {
       constexpr int M = decltype(m)::value;
-      if (fast) {
+      if (dense == 2) {
+        switch (kk) {
+          case 4: return f(&dense_kernel<SA, SB, T::C, M, 4>);
+          case 8: return f(&dense_kernel<SA, SB, T::C, M, 8>);
+          default: return f(&dense_kernel<SA, SB, T::C, M, 16>);
+        }
+      }
+      if (dense == 1) {
         switch (kk) {
           case 4: return f(&tile_kernel<SA, SB, T::C, M, 4>);
           case 8: return f(&tile_kernel<SA, SB, T::C, M, 8>);
@@ -44,7 +53,7 @@ int carveout() {
 
 cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                         cudaStream_t s) {
-  return with_smem(ka, kb, mode, p.dense != 0, p.ept, [&](auto fn) {
+  return with_smem(ka, kb, mode, p.dense, p.ept, [&](auto fn) {
     if (l.smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
       if (e != cudaSuccess) return e;
@@ -55,9 +64,9 @@ cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Lau
   });
 }
 
-int occupancy_smem(int ka, int kb, int mode, bool fast, int ept, int block, int smem) {
+int occupancy_smem(int ka, int kb, int mode, int dense, int ept, int block, int smem) {
   int n = 0;
-  with_smem(ka, kb, mode, fast, ept, [&](auto fn) {
+  with_smem(ka, kb, mode, dense, ept, [&](auto fn) {
     if (carveout() >= 0)
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout());
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

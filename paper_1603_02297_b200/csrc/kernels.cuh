@@ -592,3 +592,4 @@ __device__ __forceinline__ void cp_async_wait() {
 }  // namespace ttb
 
 #include "tile.cuh"
+#include "dense.cuh"

@@ -20,7 +20,7 @@ cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Lau
 // resident CTAs per SM for a variant (cudaOccupancyMaxActiveBlocksPerMultiprocessor)
 int occupancy_copy(int ka, int kb, int v, int mode, bool long_rows, int block);
 int occupancy_rt(int ka, int kb, int mx, int my, int mode, int block);
-int occupancy_smem(int ka, int kb, int mode, bool dense, int ept, int block, int smem);
+int occupancy_smem(int ka, int kb, int mode, int dense, int ept, int block, int smem);
 
 // data utilities (util.cu)
 struct BoxParams {

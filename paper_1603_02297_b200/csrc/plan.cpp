@@ -601,8 +601,15 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     if (m.dense) {
       const uint32_t LR = m.S * m.tx, LC = m.S * m.ty, L = m.S * m.tx * m.ty;
       const uint32_t kk = L / 256;
-      if (256 % LR == 0 && 256 % LC == 0 && L == 256 * kk && (kk == 4 || kk == 8 || kk == 16))
+      if (256 % LR == 0 && 256 % LC == 0 && L == 256 * kk && (kk == 4 || kk == 8 || kk == 16)) {
         m.ept = static_cast<int>(kk);
+        // S == 1 with both groups contiguous: the dense_kernel fast path
+        if (m.S == 1 && x_dense_in_a(g, xs) && y_dense_in_b(g, ys)) {
+          m.dense = 2;
+          while ((1u << m.ltx) < m.tx) ++m.ltx;
+          while ((1u << m.lty) < m.ty) ++m.lty;
+        }
+      }
     }
     m.rl = best_row_length(m.S, m.tx, m.ty, g.eA);
     m.dS = Div32::make(m.S);
@@ -618,12 +625,12 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     m.items = static_cast<uint32_t>(items);
     const auto r16 = [](int64_t v) { return (v + 15) & ~int64_t{15}; };
     const int64_t smem =
-        m.dense ? 2 * (r16(static_cast<int64_t>(m.tx + m.ty) * 8) +
+        m.dense ? 2 * (r16(static_cast<int64_t>(m.tx + m.ty) * (m.dense == 2 ? 4 : 8)) +
                        r16(static_cast<int64_t>(m.ty) * m.rl * g.eA))  // double-buffered
                 : static_cast<int64_t>(m.tx + m.ty) * 2 * 8 + static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);
-    const int occ = std::min(occ_cap, std::max(1, occupancy_smem(g.ka, g.kb, g.mode, m.dense != 0,
+    const int occ = std::min(occ_cap, std::max(1, occupancy_smem(g.ka, g.kb, g.mode, m.dense,
                                                                  m.ept, 256, p.l.smem)));
     p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(m.items, int64_t{occ} * sms)));
     p.a_align = std::min(16, g.eA);  // whole elements (Vec<SA, C>) move as a unit

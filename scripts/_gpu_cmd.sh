@@ -1,2 +1,7 @@
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_gpu.log
-for c in c4s c5_t00 c5_t02 c5_t06 c5_t08 c5_t10 c5_t12 c5_t14 c5_t16 c5_t18 c5_t20 c5_t22; do timeout 120 python scripts/run_case.py $c --iters 5 --check; done > gpurun_out/cases.log 2>&1
+L=paper_1603_02297_b200/_lib
+for cp in "c5_t00 kern=smem;kx=2;ky=2;tx=64;ty=64;order=1;occ=0" "c5_t16 kern=smem;kx=2;ky=1;tx=64;ty=64;order=0;occ=0" "c5_t22 kern=smem;kx=1;ky=1;tx=16;ty=128;order=0;occ=0"; do
+  set -- $cp
+  timeout 300 python scripts/ab_libs.py $1 "$2" $L/libttb.so $L/libttb_mb1.so
+done > gpurun_out/ab.log 2>&1
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err

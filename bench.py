@@ -250,7 +250,9 @@ def _strides(ext):
 
 
 def variant_of(plan_text):
-    return plan_text.split(";")[0].split("=")[1]
+    """Kernel that runs a plan: the `fn` key of ttb_plan_describe."""
+    kv = dict(p.split("=", 1) for p in plan_text.split(";") if "=" in p)
+    return kv.get("fn", kv.get("kern", "?"))
 
 
 # ------------------------------------------------------------ reference arm --
@@ -419,9 +421,16 @@ def run_engine_arm(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    ndev = torch.cuda.device_count()
+    # NCCL over NVLink when every rank has its own GPU; gloo (host) when ranks
+    # share a device (logic checks only -- the data path never communicates)
+    backend = "nccl" if ndev >= world else "gloo"
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(local % ndev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     else:
         torch.cuda.set_device(0)
     import paper_1603_02297_b200 as ttb
@@ -429,6 +438,7 @@ def run_engine_arm(args):
 
     peak, peak_kind = peaks()
     golden = golden_checksums()
+    coll_dev = "cuda" if backend == "nccl" else "cpu"
 
     def barrier():
         if world > 1:
@@ -438,7 +448,7 @@ def run_engine_arm(args):
     def allmax(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -474,8 +484,9 @@ def run_engine_arm(args):
     row_ms = [0.0] * len(rows)
     step_ms = []
     launches0 = ttb.launch_count()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local % ndev) as clk:
         barrier()
+        torch.cuda.nvtx.range_push("ttb_timed")  # ncu --nvtx-include "ttb_timed/"
         for _ in range(args.steps):
             e_start.record(stream)
             for i, r in enumerate(rows):
@@ -487,6 +498,7 @@ def run_engine_arm(args):
             step_ms.append(e_start.elapsed_time(e_stop))
             for i in range(len(rows)):
                 row_ms[i] += ev[i][0].elapsed_time(ev[i][1])
+        torch.cuda.nvtx.range_pop()
         barrier()
     launches = ttb.launch_count() - launches0
     local_ms = sum(step_ms) / len(step_ms)
@@ -518,7 +530,7 @@ def run_engine_arm(args):
         r.free()
     torch.cuda.empty_cache()
     # end-to-end through the public API with pinned host buffers
-    e2e = run_e2e(torch, ttb, rows, world, allmax, steps=min(args.steps, 2))
+    e2e = None if args.no_e2e else run_e2e(torch, ttb, rows, world, allmax, steps=min(args.steps, 2))
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
@@ -533,7 +545,8 @@ def run_engine_arm(args):
     }
     torch.cuda.empty_cache()
     if rank == 0 and world == 1:
-        line["configs"] = bench_configs(torch, ttb, peak, d2d)
+        if not args.no_configs:
+            line["configs"] = bench_configs(torch, ttb, peak, d2d)
         if not args.no_cpu:
             try:
                 kind = "reference" if _oracle().have_ref() else "port"
@@ -616,6 +629,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ttb", choices=["ttb", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (profiling runs)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the c1-c4s block (profiling runs)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")

@@ -314,6 +314,7 @@ bool Spec::parse(const std::string& s, Spec* out) {
     const auto eq = kv.find('=');
     if (eq == std::string::npos) return false;
     const std::string k = kv.substr(0, eq), v = kv.substr(eq + 1);
+    if (k == "fn") continue;  // informational (ttb_plan_describe)
     if (k == "kern") {
       have_kern = true;
       if (v == "copy")

@@ -19,11 +19,16 @@ cudaError_t with_smem(int ka, int kb, int mode, int dense, int kk, F&& f) {
     using SB = typename T::SB;
     return with_mode(mode, [&](auto m) {
       constexpr int M = decltype(m)::value;
-      if (dense == 2) {
+      if (dense == 2 || dense == 3) {  // 3: three-stage cp.async ring
+        const bool s3 = dense == 3;
         switch (kk) {
-          case 4: return f(&dense_kernel<SA, SB, T::C, M, 4>);
-          case 8: return f(&dense_kernel<SA, SB, T::C, M, 8>);
-          default: return f(&dense_kernel<SA, SB, T::C, M, 16>);
+          case 4:
+            return s3 ? f(&dense_kernel<SA, SB, T::C, M, 4, 3>) : f(&dense_kernel<SA, SB, T::C, M, 4, 2>);
+          case 8:
+            return s3 ? f(&dense_kernel<SA, SB, T::C, M, 8, 3>) : f(&dense_kernel<SA, SB, T::C, M, 8, 2>);
+          default:
+            return s3 ? f(&dense_kernel<SA, SB, T::C, M, 16, 3>)
+                      : f(&dense_kernel<SA, SB, T::C, M, 16, 2>);
         }
       }
       if (dense == 1) {

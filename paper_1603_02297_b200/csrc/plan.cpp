@@ -257,7 +257,20 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
   }
   std::stable_sort(cand.begin(), cand.end(),
                    [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
-  for (size_t i = 0; i < cand.size() && i < 8; ++i) out->push_back(cand[i]);
+  for (size_t i = 0; i < cand.size() && i < 8; ++i) {
+    out->push_back(cand[i]);
+    // power-of-two tiles of 4-16 warps' worth may run on dense_kernel: offer
+    // its three-stage cp.async ring as well (prepare() decides applicability)
+    const Spec& c = cand[i];
+    const int64_t L = S * c.tx * c.ty;
+    if (!shared && !(c.tx & (c.tx - 1)) && !(c.ty & (c.ty - 1)) && c.tx <= 256 && c.ty <= 256 &&
+        (L == 1024 || L == 2048 || L == 4096)) {
+      Spec s3 = c;
+      s3.st = 3;
+      s3.cost -= 0.05;
+      out->push_back(s3);
+    }
+  }
 }
 
 }  // namespace
@@ -299,8 +312,8 @@ std::string Spec::text() const {
                     w2, lx, kx, ky, order, occ);
       break;
     default:
-      std::snprintf(buf, sizeof buf, "kern=smem;kx=%d;ky=%d;tx=%d;ty=%d;order=%d;occ=%d", kx, ky,
-                    tx, ty, order, occ);
+      std::snprintf(buf, sizeof buf, "kern=smem;kx=%d;ky=%d;tx=%d;ty=%d;order=%d;occ=%d;st=%d", kx,
+                    ky, tx, ty, order, occ, st);
   }
   return buf;
 }
@@ -348,6 +361,8 @@ bool Spec::parse(const std::string& s, Spec* out) {
       p.order = static_cast<int>(x);
     else if (k == "occ")
       p.occ = static_cast<int>(x);
+    else if (k == "st")
+      p.st = static_cast<int>(x);
     else
       return false;
   }
@@ -606,7 +621,7 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
         m.ept = static_cast<int>(kk);
         // S == 1 with both groups contiguous: the dense_kernel fast path
         if (m.S == 1 && x_dense_in_a(g, xs) && y_dense_in_b(g, ys)) {
-          m.dense = 2;
+          m.dense = s.st >= 3 ? 3 : 2;  // 3: three-stage cp.async ring
           while ((1u << m.ltx) < m.tx) ++m.ltx;
           while ((1u << m.lty) < m.ty) ++m.lty;
         }
@@ -626,8 +641,9 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     m.items = static_cast<uint32_t>(items);
     const auto r16 = [](int64_t v) { return (v + 15) & ~int64_t{15}; };
     const int64_t smem =
-        m.dense ? 2 * (r16(static_cast<int64_t>(m.tx + m.ty) * (m.dense == 2 ? 4 : 8)) +
-                       r16(static_cast<int64_t>(m.ty) * m.rl * g.eA))  // double-buffered
+        m.dense ? (m.dense == 3 ? 3 : 2) *  // pipeline stages
+                      (r16(static_cast<int64_t>(m.tx + m.ty) * (m.dense >= 2 ? 4 : 8)) +
+                       r16(static_cast<int64_t>(m.ty) * m.rl * g.eA))
                 : static_cast<int64_t>(m.tx + m.ty) * 2 * 8 + static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);

@@ -40,6 +40,7 @@ struct Spec {
   int tx = 0, ty = 0;  // smem tile extents along X / Y
   int order = 0;       // 0: X chunks fastest, 1: Y chunks fastest
   int occ = 0;         // CTAs per SM (0: occupancy limit)
+  int st = 2;          // smem: cp.async pipeline stages (dense tiles: 2 or 3)
   double cost = 0;     // heuristic rank (lower first)
 
   std::string text() const;

@@ -88,13 +88,65 @@ __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == size
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
       const uint32_t y = yl + k * R;  // < ty: the table read is in bounds even when masked
+#ifndef TTB_EXP_NOLOAD  // experiment switch: time the store side alone
       cp_async_pred<EB>(dst + k * R * P.rl, ax + ra[y], xv && y < t.ny);
+#endif
     }
   };
 
   const uint32_t g = gridDim.x;
   uint32_t it = blockIdx.x;
   if (it >= P.items) return;
+#ifdef TTB_EXP_REGLOAD
+  // experiment: register double buffering (LDG next tile, store current, STS)
+  {
+    const uint32_t yt = threadIdx.x & (P.ty - 1), xt = threadIdx.x >> P.lty;
+    const uint32_t Q = 256u >> P.lty;
+    E rg[EPT];
+    auto ldg = [&](const DenseTile& t, int s) {
+      const uint32_t* ra = rowA(s);
+      const bool xv = xl < t.nx;
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const uint32_t y = yl + k * R;
+        vload_b_pred(rg[k], (A + xl + ra[y])->v, xv && y < t.ny);
+      }
+    };
+    auto sts = [&](int s) {
+      E* dst = tile(s) + yl * P.rl + xl;
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) dst[k * R * P.rl] = rg[k];
+    };
+    tables(dense_tile(P, it), 0);
+    __syncthreads();
+    ldg(dense_tile(P, it), 0);
+    sts(0);
+    __syncthreads();
+    for (int s = 0; it < P.items; it += g, s ^= 1) {
+      const uint32_t nxt = it + g;
+      if (nxt < P.items) tables(dense_tile(P, nxt), s ^ 1);
+      __syncthreads();
+      if (nxt < P.items) ldg(dense_tile(P, nxt), s ^ 1);
+      const DenseTile cur = dense_tile(P, it);
+      const uint32_t* cb = colB(s);
+      const bool yv = yt < cur.ny;
+      EBv* by = B + yt;
+      const E* src = tile(s) + yt * P.rl + xt;
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const uint32_t x = xt + k * Q;
+        EBv w;
+        const E a = src[k * Q];
+#pragma unroll
+        for (int c = 0; c < C; ++c) w.v[c] = up(a.v[c], w.v[c]);
+        vstore_pred((by + cb[x])->v, w, yv && x < cur.nx);
+      }
+      if (nxt < P.items) sts(s ^ 1);
+      __syncthreads();
+    }
+    return;
+  }
+#endif
   // prologue: tables and loads of the first NS-1 tiles
 #pragma unroll
   for (int p = 0; p < NS - 1; ++p)
@@ -121,6 +173,41 @@ __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == size
     // smem -> B: B-contiguous walk (y fastest)
     const DenseTile cur = dense_tile(P, it);
     const uint32_t* cb = colB(s);
+#ifdef TTB_EXP_ALIGNED_STORE
+    // Experiment (measured slower, kept for reference): line-aligned column
+    // stores.  Sequential per-warp columns lose the store-level parallelism of
+    // the batched walk below, which outweighs the saved L2 transactions.
+    if (P.ty >= 32) {
+      // Line-aligned column stores: warp w writes columns w, w+8, ...; its
+      // lanes cover 32 consecutive B elements starting at a multiple of 32
+      // elements in memory (shifted by the column's misalignment), so every
+      // warp store touches whole aligned lines and never straddles two --
+      // misaligned 32-element stores cost twice the L2 write transactions.
+      const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      const E* tl = tile(s);
+      for (uint32_t x = warp; x < cur.nx; x += 8) {
+        const uint32_t base = cb[x];
+        // misalignment (elements) of y = 0 within its 32-element memory span
+        const uint32_t d = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(B + base) / sizeof(EBv)) & 31u;
+        EBv* col = B + (base - d);
+        const uint32_t spans = (cur.ny + d + 31) >> 5;
+        for (uint32_t j = 0; j < spans; ++j) {
+          const int32_t y = static_cast<int32_t>(j * 32 + lane) - static_cast<int32_t>(d);
+          const bool v = y >= 0 && y < static_cast<int32_t>(cur.ny);
+          const uint32_t yc = v ? static_cast<uint32_t>(y) : 0u;
+          EBv w;
+          EBv* q = col + j * 32 + lane;
+          if constexpr (MODE == 2) vload_b_pred(w, q->v, v);
+          const E a = tl[yc * P.rl + x];
+#pragma unroll
+          for (int c = 0; c < C; ++c) w.v[c] = up(a.v[c], w.v[c]);
+          vstore_pred(q->v, w, v);
+        }
+      }
+      __syncthreads();
+      continue;
+    }
+#endif
     const bool yv = yt < cur.ny;
     EBv* by = B + yt;
     const E* src = tile(s) + yt * P.rl + xt;
@@ -143,7 +230,11 @@ __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == size
       for (int u = 0; u < U; ++u) {
 #pragma unroll
         for (int c = 0; c < C; ++c) w[u].v[c] = up(a[u].v[c], w[u].v[c]);
+#ifndef TTB_EXP_NOSTORE  // experiment switch: time the load side alone
         vstore_pred(q[u]->v, w[u], v[u]);
+#else
+        if (a[u].v[0] == SA(12345.678)) vstore_pred(q[u]->v, w[u], v[u]);  // keep the reads live
+#endif
       }
     }
     __syncthreads();

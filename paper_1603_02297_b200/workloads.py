@@ -95,4 +95,13 @@ C5: List[Workload] = [
 ]
 
 ALL: List[Workload] = CONFIGS + C5
-BY_NAME = {w.name: w for w in ALL}
+
+# kernel-tuning probes (not BASELINE configs): the c5 t=0 permutation with
+# sector-aligned and unaligned leading extents
+PROBES: List[Workload] = [
+    Workload("p_t00_a80", "s", (3, 2, 0, 4, 1), (80, 42, 11, 248, 44), 1.0, 0.0, 7000),
+    Workload("p_t00_a79", "s", (3, 2, 0, 4, 1), (79, 42, 11, 245, 45), 1.0, 0.0, 7001),
+    Workload("p_copy_a", "s", (0, 1), (1 << 15, 12288), 1.0, 0.0, 7002),
+]
+
+BY_NAME = {w.name: w for w in ALL + PROBES}

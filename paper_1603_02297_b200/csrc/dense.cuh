@@ -6,8 +6,10 @@
 // predicated cp.async (load) or store.  NS tile stages form a cp.async ring:
 // the loads of the next NS-1 tiles are in flight while the current tile is
 // written out, which is what keeps enough bytes in flight per SM (Little's
-// law) at the low occupancy these unrolled walks allow.  Everything that is
-// not a power-of-two dense tile runs on tile_kernel (tile.cuh).
+// law) at the low occupancy these unrolled walks allow.  With beta != 0 the
+// tile's B elements ride the same ring (second smem buffer), so the
+// read-modify-write of B never waits on HBM latency.  Everything that is not
+// a power-of-two dense tile runs on tile_kernel (tile.cuh).
 #pragma once
 
 #include "kernels.cuh"
@@ -39,6 +41,15 @@ __device__ __forceinline__ DenseTile dense_tile(const SmemParams& P, uint32_t it
   return t;
 }
 
+// bytes of one pipeline stage; must match plan.cpp's shared-memory size
+__host__ __device__ inline uint32_t dense_stage_bytes(uint32_t tx, uint32_t ty, uint32_t rl,
+                                                      uint32_t ea, uint32_t eb, int mode) {
+  const uint32_t tables = ((tx + ty) * 4 + 15) & ~15u;
+  const uint32_t tile_a = (ty * rl * ea + 15) & ~15u;
+  const uint32_t tile_b = mode == 2 ? ((tx * ty * eb + 15) & ~15u) : 0u;
+  return tables + tile_a + tile_b;
+}
+
 template <class SA, class SB, int C, int MODE, int EPT, int NS>
 __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == sizeof(SB))
                                            ? 1
@@ -47,14 +58,19 @@ __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == size
   using E = Vec<SA, C>;
   using EBv = Vec<SB, C>;
   constexpr int EB = static_cast<int>(sizeof(E));
+  constexpr int EBB = static_cast<int>(sizeof(EBv));
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // offsets are 32-bit: the planner only picks this kernel for tensors whose
   // footprints stay below 2^31 elements
   const uint32_t table_bytes = ((P.tx + P.ty) * 4 + 15) & ~15u;
-  const uint32_t stage_bytes = table_bytes + ((P.ty * P.rl * EB + 15) & ~15u);
+  const uint32_t tile_a_bytes = (P.ty * P.rl * EB + 15) & ~15u;
+  const uint32_t stage_bytes = dense_stage_bytes(P.tx, P.ty, P.rl, EB, EBB, MODE);
   auto rowA = [&](int s) { return reinterpret_cast<uint32_t*>(smem_raw + s * stage_bytes); };
   auto colB = [&](int s) { return rowA(s) + P.ty; };
   auto tile = [&](int s) { return reinterpret_cast<E*>(smem_raw + s * stage_bytes + table_bytes); };
+  auto tileB = [&](int s) {  // [x][y], column-major like B
+    return reinterpret_cast<EBv*>(smem_raw + s * stage_bytes + table_bytes + tile_a_bytes);
+  };
 
   const Update<SA, SB, MODE> up(P.sc);
   const E* __restrict__ A = static_cast<const E*>(P.A);
@@ -77,9 +93,12 @@ __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == size
       cb[i] = static_cast<uint32_t>(b + bO + t.y0);
     }
   };
-  // A -> smem: A-contiguous walk (x fastest), all of it asynchronous
+  // load walk: thread column xl, rows yl + k*R (A-contiguous along x)
   const uint32_t xl = threadIdx.x & (P.tx - 1), yl = threadIdx.x >> P.ltx;
   const uint32_t R = 256u >> P.ltx;
+  // store walk: thread row yt, columns xt + k*Q (B-contiguous along y)
+  const uint32_t yt = threadIdx.x & (P.ty - 1), xt = threadIdx.x >> P.lty;
+  const uint32_t Q = 256u >> P.lty;
   auto loads = [&](const DenseTile& t, int s) {
     const uint32_t* ra = rowA(s);
     const bool xv = xl < t.nx;
@@ -92,61 +111,22 @@ __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == size
       cp_async_pred<EB>(dst + k * R * P.rl, ax + ra[y], xv && y < t.ny);
 #endif
     }
+    if constexpr (MODE == 2) {  // the tile's B elements, in the store walk's layout
+      const uint32_t* cb = colB(s);
+      const bool yv = yt < t.ny;
+      EBv* bdst = tileB(s) + yt;
+      const EBv* by = B + yt;
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const uint32_t x = xt + k * Q;
+        cp_async_pred<EBB>(bdst + x * P.ty, by + cb[x], yv && x < t.nx);
+      }
+    }
   };
 
   const uint32_t g = gridDim.x;
   uint32_t it = blockIdx.x;
   if (it >= P.items) return;
-#ifdef TTB_EXP_REGLOAD
-  // experiment: register double buffering (LDG next tile, store current, STS)
-  {
-    const uint32_t yt = threadIdx.x & (P.ty - 1), xt = threadIdx.x >> P.lty;
-    const uint32_t Q = 256u >> P.lty;
-    E rg[EPT];
-    auto ldg = [&](const DenseTile& t, int s) {
-      const uint32_t* ra = rowA(s);
-      const bool xv = xl < t.nx;
-#pragma unroll
-      for (int k = 0; k < EPT; ++k) {
-        const uint32_t y = yl + k * R;
-        vload_b_pred(rg[k], (A + xl + ra[y])->v, xv && y < t.ny);
-      }
-    };
-    auto sts = [&](int s) {
-      E* dst = tile(s) + yl * P.rl + xl;
-#pragma unroll
-      for (int k = 0; k < EPT; ++k) dst[k * R * P.rl] = rg[k];
-    };
-    tables(dense_tile(P, it), 0);
-    __syncthreads();
-    ldg(dense_tile(P, it), 0);
-    sts(0);
-    __syncthreads();
-    for (int s = 0; it < P.items; it += g, s ^= 1) {
-      const uint32_t nxt = it + g;
-      if (nxt < P.items) tables(dense_tile(P, nxt), s ^ 1);
-      __syncthreads();
-      if (nxt < P.items) ldg(dense_tile(P, nxt), s ^ 1);
-      const DenseTile cur = dense_tile(P, it);
-      const uint32_t* cb = colB(s);
-      const bool yv = yt < cur.ny;
-      EBv* by = B + yt;
-      const E* src = tile(s) + yt * P.rl + xt;
-#pragma unroll
-      for (int k = 0; k < EPT; ++k) {
-        const uint32_t x = xt + k * Q;
-        EBv w;
-        const E a = src[k * Q];
-#pragma unroll
-        for (int c = 0; c < C; ++c) w.v[c] = up(a.v[c], w.v[c]);
-        vstore_pred((by + cb[x])->v, w, yv && x < cur.nx);
-      }
-      if (nxt < P.items) sts(s ^ 1);
-      __syncthreads();
-    }
-    return;
-  }
-#endif
   // prologue: tables and loads of the first NS-1 tiles
 #pragma unroll
   for (int p = 0; p < NS - 1; ++p)
@@ -158,8 +138,6 @@ __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == size
     cp_async_commit();
   }
 
-  const uint32_t yt = threadIdx.x & (P.ty - 1), xt = threadIdx.x >> P.lty;
-  const uint32_t Q = 256u >> P.lty;
   for (int s = 0; it < P.items; it += g, s = (s + 1 == NS) ? 0 : s + 1) {
     const uint32_t nxt = it + (NS - 1) * g;
     const int sn = (s + NS - 1) % NS;  // the stage tile it - g used
@@ -173,44 +151,10 @@ __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == size
     // smem -> B: B-contiguous walk (y fastest)
     const DenseTile cur = dense_tile(P, it);
     const uint32_t* cb = colB(s);
-#ifdef TTB_EXP_ALIGNED_STORE
-    // Experiment (measured slower, kept for reference): line-aligned column
-    // stores.  Sequential per-warp columns lose the store-level parallelism of
-    // the batched walk below, which outweighs the saved L2 transactions.
-    if (P.ty >= 32) {
-      // Line-aligned column stores: warp w writes columns w, w+8, ...; its
-      // lanes cover 32 consecutive B elements starting at a multiple of 32
-      // elements in memory (shifted by the column's misalignment), so every
-      // warp store touches whole aligned lines and never straddles two --
-      // misaligned 32-element stores cost twice the L2 write transactions.
-      const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      const E* tl = tile(s);
-      for (uint32_t x = warp; x < cur.nx; x += 8) {
-        const uint32_t base = cb[x];
-        // misalignment (elements) of y = 0 within its 32-element memory span
-        const uint32_t d = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(B + base) / sizeof(EBv)) & 31u;
-        EBv* col = B + (base - d);
-        const uint32_t spans = (cur.ny + d + 31) >> 5;
-        for (uint32_t j = 0; j < spans; ++j) {
-          const int32_t y = static_cast<int32_t>(j * 32 + lane) - static_cast<int32_t>(d);
-          const bool v = y >= 0 && y < static_cast<int32_t>(cur.ny);
-          const uint32_t yc = v ? static_cast<uint32_t>(y) : 0u;
-          EBv w;
-          EBv* q = col + j * 32 + lane;
-          if constexpr (MODE == 2) vload_b_pred(w, q->v, v);
-          const E a = tl[yc * P.rl + x];
-#pragma unroll
-          for (int c = 0; c < C; ++c) w.v[c] = up(a.v[c], w.v[c]);
-          vstore_pred(q->v, w, v);
-        }
-      }
-      __syncthreads();
-      continue;
-    }
-#endif
     const bool yv = yt < cur.ny;
     EBv* by = B + yt;
     const E* src = tile(s) + yt * P.rl + xt;
+    const EBv* bsrc = tileB(s) + yt;
     constexpr int U = EPT < 8 ? EPT : 8;
 #pragma unroll
     for (int k0 = 0; k0 < EPT; k0 += U) {
@@ -223,7 +167,7 @@ __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == size
         const uint32_t x = xt + (k0 + u) * Q;  // < tx: table read in bounds when masked
         v[u] = yv && x < cur.nx;
         q[u] = by + cb[x];
-        if constexpr (MODE == 2) vload_b_pred(w[u], q[u]->v, v[u]);
+        if constexpr (MODE == 2) w[u] = bsrc[x * P.ty];
         a[u] = src[(k0 + u) * Q];
       }
 #pragma unroll

@@ -641,9 +641,10 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     m.items = static_cast<uint32_t>(items);
     const auto r16 = [](int64_t v) { return (v + 15) & ~int64_t{15}; };
     const int64_t smem =
-        m.dense ? (m.dense == 3 ? 3 : 2) *  // pipeline stages
+        m.dense ? (m.dense == 3 ? 3 : 2) *  // pipeline stages (dense_stage_bytes in dense.cuh)
                       (r16(static_cast<int64_t>(m.tx + m.ty) * (m.dense >= 2 ? 4 : 8)) +
-                       r16(static_cast<int64_t>(m.ty) * m.rl * g.eA))
+                       r16(static_cast<int64_t>(m.ty) * m.rl * g.eA) +
+                       (g.mode == 2 ? r16(static_cast<int64_t>(m.S) * m.tx * m.ty * g.eB) : 0))
                 : static_cast<int64_t>(m.tx + m.ty) * 2 * 8 + static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);

@@ -55,12 +55,19 @@ __global__ void __launch_bounds__(256, KK > 0 ? TTB_TILE_MINB : 1) tile_kernel(c
   using EA = Vec<SA, C>;
   using EBv = Vec<SB, C>;
   constexpr int EAB = static_cast<int>(sizeof(EA));
+  constexpr int EBB = static_cast<int>(sizeof(EBv));
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // per stage: offAX[tx] offBX[tx] offAY[ty] offBY[ty] (uint32), then the tile
+  // per stage: offAX[tx] offBX[tx] offAY[ty] offBY[ty] (uint32), the A tile,
+  // and with beta != 0 the tile's B elements ([x][s, y], prefetched by cp.async)
   const uint32_t table_bytes = ((P.tx + P.ty) * 8 + 15) & ~15u;
-  const uint32_t stage_bytes = table_bytes + ((P.ty * P.rl * EAB + 15) & ~15u);
+  const uint32_t tile_a_bytes = (P.ty * P.rl * EAB + 15) & ~15u;
+  const uint32_t stage_bytes =
+      table_bytes + tile_a_bytes + (MODE == 2 ? ((P.S * P.tx * P.ty * EBB + 15) & ~15u) : 0u);
   auto tab = [&](int s) { return reinterpret_cast<uint32_t*>(smem_raw + s * stage_bytes); };
   auto tile = [&](int s) { return reinterpret_cast<EA*>(smem_raw + s * stage_bytes + table_bytes); };
+  auto tileB = [&](int s) {
+    return reinterpret_cast<EBv*>(smem_raw + s * stage_bytes + table_bytes + tile_a_bytes);
+  };
 
   const Update<SA, SB, MODE> up(P.sc);
   const EA* __restrict__ A = static_cast<const EA*>(P.A);
@@ -112,6 +119,21 @@ __global__ void __launch_bounds__(256, KK > 0 ? TTB_TILE_MINB : 1) tile_kernel(c
         cp_async_pred<EAB>(dst + k * R * P.rl, a0 + offAY[KK > 0 ? y : min(y, P.ty - 1)], v);
       }
     }
+    if constexpr (MODE == 2) {  // B elements of the tile, in the store walk's layout
+      const bool vy = act_s && y_s < t.ny;
+      const EBv* b0 = B + (vy ? T[2 * P.tx + P.ty + y_s] : 0u) + s_s;
+      const uint32_t* offBX = T + P.tx;
+      EBv* bdst = tileB(s) + j_s;
+      for (uint32_t k0 = 0; k0 < K2; k0 += UN) {
+#pragma unroll
+        for (uint32_t u = 0; u < UN; ++u) {
+          const uint32_t k = k0 + u;
+          const uint32_t x = c0 + k * Q;
+          const uint32_t xc = KK > 0 ? x : min(x, P.tx - 1);
+          cp_async_pred<EBB>(bdst + xc * LC, b0 + offBX[xc], vy && (KK > 0 || k < K2) && x < t.nx);
+        }
+      }
+    }
   };
 
   uint32_t it = blockIdx.x;
@@ -141,7 +163,8 @@ __global__ void __launch_bounds__(256, KK > 0 ? TTB_TILE_MINB : 1) tile_kernel(c
       EBv* b0 = B + (vy ? T[2 * P.tx + P.ty + y_s] : 0u) + s_s;
       const uint32_t* offBX = T + P.tx;
       const EA* src = tile(s) + y_s * P.rl + s_s;
-      constexpr uint32_t U2 = UN > 8 ? 8 : UN;  // B loads in flight per batch
+      const EBv* bsrc = tileB(s) + j_s;
+      constexpr uint32_t U2 = UN > 8 ? 8 : UN;  // stores per batch
       for (uint32_t k0 = 0; k0 < K2; k0 += U2) {
         EBv w[U2];
         EA a[U2];
@@ -154,7 +177,7 @@ __global__ void __launch_bounds__(256, KK > 0 ? TTB_TILE_MINB : 1) tile_kernel(c
           const uint32_t xc = KK > 0 ? x : min(x, P.tx - 1);
           v[u] = vy && (KK > 0 || k < K2) && x < cur.nx;
           q[u] = b0 + offBX[xc];
-          if constexpr (MODE == 2) vload_b_pred(w[u], q[u]->v, v[u]);
+          if constexpr (MODE == 2) w[u] = bsrc[xc * LC];
           a[u] = src[xc * P.S];
         }
 #pragma unroll

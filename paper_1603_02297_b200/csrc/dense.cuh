@@ -167,7 +167,8 @@ __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == size
         const uint32_t x = xt + (k0 + u) * Q;  // < tx: table read in bounds when masked
         v[u] = yv && x < cur.nx;
         q[u] = by + cb[x];
-        if constexpr (MODE == 2) w[u] = bsrc[x * P.ty];
+        if constexpr (MODE == 2) w[u] = bsrc[x * P.ty];             // prefetched
+        if constexpr (MODE == 3) vload_b_pred(w[u], q[u]->v, v[u]);  // direct (no B ring)
         a[u] = src[(k0 + u) * Q];
       }
 #pragma unroll

@@ -17,7 +17,13 @@ cudaError_t with_smem(int ka, int kb, int mode, int dense, int kk, F&& f) {
     using T = decltype(t);
     using SA = typename T::SA;
     using SB = typename T::SB;
-    return with_mode(mode, [&](auto m) {
+    // mode 3 (update with direct B reads) exists for the staged-tile kernels
+    // only; the 64-bit smem_kernel always reads B directly under mode 2
+    auto modes = [&](auto&& g) -> cudaError_t {
+      if (mode == 3) return g(std::integral_constant<int, 3>{});
+      return with_mode(mode, g);
+    };
+    return modes([&](auto m) {
       constexpr int M = decltype(m)::value;
       if (dense == 2 || dense == 3) {  // 3: three-stage cp.async ring
         const bool s3 = dense == 3;
@@ -39,7 +45,7 @@ cudaError_t with_smem(int ka, int kb, int mode, int dense, int kk, F&& f) {
           default: return f(&tile_kernel<SA, SB, T::C, M, 0>);
         }
       }
-      return f(&smem_kernel<SA, SB, T::C, M>);
+      return f(&smem_kernel<SA, SB, T::C, (M == 3 ? 2 : M)>);
     });
   });
 }

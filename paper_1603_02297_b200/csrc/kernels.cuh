@@ -58,7 +58,9 @@ __device__ __forceinline__ double narrow<double>(double x) { return x; }
 
 // Update modes: 0 = move (alpha == 1, beta == 0: SB(W(a)), no arithmetic),
 // 1 = scale (beta == 0: SB(alpha*W(a)), B never read),
-// 2 = update (SB(alpha*W(a) + beta*W(b)), two products, one sum).
+// 2 = update (SB(alpha*W(a) + beta*W(b)), two products, one sum);
+// 3 = update as well -- the staged-tile kernels use it for "read B directly
+// instead of through the cp.async ring".
 template <class SA, class SB, int MODE>
 struct Update {
   using W = typename WideOf<SA, SB>::type;

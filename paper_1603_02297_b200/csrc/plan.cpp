@@ -259,6 +259,12 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
                    [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
   for (size_t i = 0; i < cand.size() && i < 8; ++i) {
     out->push_back(cand[i]);
+    if (g.mode == 2) {  // beta != 0: also try B read directly (smaller stages, more CTAs)
+      Spec d = cand[i];
+      d.bp = 0;
+      d.cost += 0.02;
+      out->push_back(d);
+    }
     // power-of-two tiles of 4-16 warps' worth may run on dense_kernel: offer
     // its three-stage cp.async ring as well (prepare() decides applicability)
     const Spec& c = cand[i];
@@ -312,8 +318,8 @@ std::string Spec::text() const {
                     w2, lx, kx, ky, order, occ);
       break;
     default:
-      std::snprintf(buf, sizeof buf, "kern=smem;kx=%d;ky=%d;tx=%d;ty=%d;order=%d;occ=%d;st=%d", kx,
-                    ky, tx, ty, order, occ, st);
+      std::snprintf(buf, sizeof buf, "kern=smem;kx=%d;ky=%d;tx=%d;ty=%d;order=%d;occ=%d;st=%d;bp=%d",
+                    kx, ky, tx, ty, order, occ, st, bp);
   }
   return buf;
 }
@@ -363,6 +369,8 @@ bool Spec::parse(const std::string& s, Spec* out) {
       p.occ = static_cast<int>(x);
     else if (k == "st")
       p.st = static_cast<int>(x);
+    else if (k == "bp")
+      p.bp = static_cast<int>(x);
     else
       return false;
   }
@@ -493,7 +501,7 @@ std::vector<Spec> candidates(const Geo& g) {
       fallback = s;
       have_fb = true;
     }
-  if (out.size() > 16) out.resize(16);
+  if (out.size() > 24) out.resize(24);
   if (have_fb) out.push_back(fallback);
   return out;
 }
@@ -639,16 +647,18 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     const uint64_t items = uint64_t{m.nxc} * m.nyc * m.O.total;
     if (items >= kIdxLimit) return fail("smem: too many tiles");
     m.items = static_cast<uint32_t>(items);
+    // beta != 0 without the B ring: kernel mode 3 (staged-tile kernels only)
+    if (g.mode == 2 && s.bp == 0 && m.dense) p.mode = 3;
     const auto r16 = [](int64_t v) { return (v + 15) & ~int64_t{15}; };
     const int64_t smem =
         m.dense ? (m.dense == 3 ? 3 : 2) *  // pipeline stages (dense_stage_bytes in dense.cuh)
                       (r16(static_cast<int64_t>(m.tx + m.ty) * (m.dense >= 2 ? 4 : 8)) +
                        r16(static_cast<int64_t>(m.ty) * m.rl * g.eA) +
-                       (g.mode == 2 ? r16(static_cast<int64_t>(m.S) * m.tx * m.ty * g.eB) : 0))
+                       (p.mode == 2 ? r16(static_cast<int64_t>(m.S) * m.tx * m.ty * g.eB) : 0))
                 : static_cast<int64_t>(m.tx + m.ty) * 2 * 8 + static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);
-    const int occ = std::min(occ_cap, std::max(1, occupancy_smem(g.ka, g.kb, g.mode, m.dense,
+    const int occ = std::min(occ_cap, std::max(1, occupancy_smem(g.ka, g.kb, p.mode, m.dense,
                                                                  m.ept, 256, p.l.smem)));
     p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(m.items, int64_t{occ} * sms)));
     p.a_align = std::min(16, g.eA);  // whole elements (Vec<SA, C>) move as a unit

@@ -41,6 +41,7 @@ struct Spec {
   int order = 0;       // 0: X chunks fastest, 1: Y chunks fastest
   int occ = 0;         // CTAs per SM (0: occupancy limit)
   int st = 2;          // smem: cp.async pipeline stages (dense tiles: 2 or 3)
+  int bp = 1;          // smem, beta != 0: B through the cp.async ring (1) or direct (0)
   double cost = 0;     // heuristic rank (lower first)
 
   std::string text() const;

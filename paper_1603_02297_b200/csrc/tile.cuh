@@ -177,7 +177,8 @@ __global__ void __launch_bounds__(256, KK > 0 ? TTB_TILE_MINB : 1) tile_kernel(c
           const uint32_t xc = KK > 0 ? x : min(x, P.tx - 1);
           v[u] = vy && (KK > 0 || k < K2) && x < cur.nx;
           q[u] = b0 + offBX[xc];
-          if constexpr (MODE == 2) w[u] = bsrc[xc * LC];
+          if constexpr (MODE == 2) w[u] = bsrc[xc * LC];               // prefetched
+          if constexpr (MODE == 3) vload_b_pred(w[u], q[u]->v, v[u]);  // direct (no B ring)
           a[u] = src[xc * P.S];
         }
 #pragma unroll

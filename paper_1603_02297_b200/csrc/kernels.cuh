@@ -222,40 +222,50 @@ __device__ __forceinline__ bool copy_row(const CopyParams& P, uint32_t r, int64_
   return true;
 }
 
-// Shared stride-1 index, short rows: each thread moves vectors of V
-// elements, contiguous in A and B, U of them in flight.
+// Shared stride-1 index, short rows: a warp owns 32 consecutive rows (in tile
+// order).  Lane l decodes row l's offsets once; the warp then streams the
+// 32 * lvec vectors of those rows with consecutive lanes on consecutive
+// vectors, fetching each vector's row offsets by warp shuffle -- no per-vector
+// index decode.  U vectors per lane in flight.
 template <class SA, class SB, int C, int V, int MODE>
 __global__ void __launch_bounds__(256) copy_kernel(const CopyParams P) {
   const Update<SA, SB, MODE> up(P.sc);
   const SA* __restrict__ A = static_cast<const SA*>(P.A);
   SB* __restrict__ B = static_cast<SB*>(P.B);
   constexpr int U = 4;
-  const uint32_t nth = gridDim.x * blockDim.x;
-  for (uint32_t f0 = blockIdx.x * blockDim.x + threadIdx.x; f0 < P.items; f0 += U * nth) {
-    Vec<SA, V * C> a[U];
-    Vec<SB, V * C> b[U];
-    SB* pb[U];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < P.items; it += nwarps) {
+    const uint32_t r = it * 32 + lane;
+    int64_t roa = 0, rob = 0;
+    const bool rok = r < P.rows && copy_row(P, r, roa, rob);
+    for (uint32_t k0 = 0; k0 < P.lvec; k0 += U) {
+      Vec<SA, V * C> a[U];
+      Vec<SB, V * C> b[U];
+      SB* pb[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t f = f0 + u * nth;
-      pb[u] = nullptr;
-      int64_t oa, ob;
-      if (f < P.items) {
-        const uint32_t row = udiv(f, P.dl);
-        const uint32_t v = f - row * P.lvec;
-        if (copy_row(P, row, oa, ob)) {
+      for (int u = 0; u < U; ++u) {
+        const uint32_t f = (k0 + u) * 32 + lane;  // vector index within the 32 rows
+        const uint32_t rl = udiv(f, P.dl);          // row within the group (< 32 when valid)
+        const uint32_t v = f - rl * P.lvec;
+        const uint32_t src = rl & 31;
+        const int64_t oa = __shfl_sync(0xffffffffu, roa, src);
+        const int64_t ob = __shfl_sync(0xffffffffu, rob, src);
+        const bool ok = __shfl_sync(0xffffffffu, rok, src) && k0 + u < P.lvec;
+        pb[u] = nullptr;
+        if (ok) {
           vload_a(a[u], A + (oa + static_cast<int64_t>(v) * V) * C);
           pb[u] = B + (ob + static_cast<int64_t>(v) * V) * C;
           if constexpr (MODE == 2) vload_b(b[u], pb[u]);
         }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!pb[u]) continue;
+      for (int u = 0; u < U; ++u) {
+        if (!pb[u]) continue;
 #pragma unroll
-      for (int i = 0; i < V * C; ++i) b[u].v[i] = up(a[u].v[i], b[u].v[i]);
-      vstore(pb[u], b[u]);
+        for (int i = 0; i < V * C; ++i) b[u].v[i] = up(a[u].v[i], b[u].v[i]);
+        vstore(pb[u], b[u]);
+      }
     }
   }
 }

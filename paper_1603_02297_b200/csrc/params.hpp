@@ -72,7 +72,8 @@ struct CopyParams {
   int order;
   uint32_t nseg;          // row segments of 32*U vectors (long-row kernel)
   Div32 dseg;
-  uint32_t items;         // long rows: warp items; short rows: vectors (incl. masked)
+  uint32_t rows;          // rows including the masked rows of partial tiles
+  uint32_t items;         // warp items: long rows (row, segment); short rows 32-row groups
   int long_rows;          // 1: copy_rows_kernel, 0: copy_kernel
 };
 

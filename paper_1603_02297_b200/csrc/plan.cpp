@@ -551,13 +551,15 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     c.long_rows = c.lvec >= 128 ? 1 : 0;
     c.nseg = (c.lvec + kSeg - 1) / kSeg;
     c.dseg = Div32::make(c.nseg);
-    const uint64_t items = c.long_rows ? rows * c.nseg : rows * c.lvec;
-    if (rows >= kIdxLimit || items >= kIdxLimit) return fail("copy: index space exceeds 2^31");
+    // warp items: (row, segment) for long rows, groups of 32 rows for short ones
+    const uint64_t items = c.long_rows ? rows * c.nseg : (rows + 31) / 32;
+    if (rows >= kIdxLimit || items >= kIdxLimit || uint64_t{32} * c.lvec >= kIdxLimit)
+      return fail("copy: index space exceeds 2^31");
+    c.rows = static_cast<uint32_t>(rows);
     c.items = static_cast<uint32_t>(items);
     const int occ = std::min(
         occ_cap, std::max(1, occupancy_copy(g.ka, g.kb, v, g.mode, c.long_rows != 0, 256)));
-    const int64_t want = c.long_rows ? (static_cast<int64_t>(c.items) + 7) / 8
-                                     : (static_cast<int64_t>(c.items) + 256 * 4 - 1) / (256 * 4);
+    const int64_t want = (static_cast<int64_t>(c.items) + 7) / 8;
     p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t{occ} * sms)));
     p.a_align = v * g.eA;
     p.b_align = v * g.eB;

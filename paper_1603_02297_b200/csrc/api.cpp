@@ -80,11 +80,18 @@ struct ttb_plan_s {
   // end-to-end staging (ttb_plan_execute_host)
   void* dA = nullptr;
   void* dB = nullptr;
-  cudaStream_t hs = nullptr;
+  cudaStream_t hs = nullptr;  // host->device copies
+  cudaStream_t ks = nullptr;  // slab kernels (pipelined path)
+  cudaStream_t ds = nullptr;  // device->host copies (pipelined path)
+  std::vector<cudaEvent_t> evs;
+  std::unordered_map<int64_t, std::unique_ptr<ttb_plan_s>> chunk_plans;  // by slab extent
   ~ttb_plan_s() {
     if (dA) cudaFree(dA);
     if (dB) cudaFree(dB);
     if (hs) cudaStreamDestroy(hs);
+    if (ks) cudaStreamDestroy(ks);
+    if (ds) cudaStreamDestroy(ds);
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
   }
   size_t bytes_a() const { return static_cast<size_t>(orig.footprint_a()) * kind_bytes(orig.kind_a); }
   size_t bytes_b() const { return static_cast<size_t>(orig.footprint_b()) * kind_bytes(orig.kind_b); }
@@ -199,6 +206,178 @@ int box_params(int kind, int rank, const int64_t* sizes, const int64_t* ld, cons
     bp->total *= sizes[d];
   }
   return TTB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined host path.  PCIe is full duplex (both directions at once measure
+// ~2x one direction), so ttb_plan_execute_host cuts the problem into K slabs
+// along one (merged) axis `a`: slab i's A part streams in on one copy engine,
+// its kernel runs, and its B part streams out on the other while slab i+1
+// streams in.  A slab is, on each side, `height` rows of `width` bytes at a
+// fixed pitch: the axis is chosen so that every axis above it on that side is
+// unpadded (a 2D copy) and the rows are long enough for the copy engines.
+
+bool pinned(const void* p) {
+  cudaPointerAttributes at{};
+  const bool ok = cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // a pageable pointer can leave "invalid value" behind
+  return ok;
+}
+
+struct SlabSide {
+  int64_t stride = 0;  // elements between consecutive indices of the slab axis
+  int64_t pitch = 0;   // elements between rows
+  int64_t height = 1;  // rows
+  int64_t foot = 0;    // required elements of the whole buffer
+  int eb = 4;          // element bytes
+};
+
+struct HostPipe {
+  int axis = 0;        // merged A axis the slabs cut
+  int64_t n = 0, ext = 0;
+  SlabSide a, b;
+  bool b_in = false;   // B slabs travel to the device too (beta != 0 or padded below the axis)
+};
+
+// rows of one side for slab axis extent at position `q` of the side's order
+bool slab_side(const std::vector<int64_t>& n, const std::vector<int64_t>& ld, int q, int eb,
+               int64_t foot, SlabSide* out) {
+  const int r = static_cast<int>(n.size());
+  int64_t st = 1;
+  for (int k = 0; k < q; ++k) st *= ld[static_cast<size_t>(k)];
+  out->stride = st;
+  out->pitch = st * ld[static_cast<size_t>(q)];
+  out->height = 1;
+  for (int k = q + 1; k < r; ++k) {
+    if (k < r - 1 && ld[static_cast<size_t>(k)] != n[static_cast<size_t>(k)]) return false;
+    out->height *= n[static_cast<size_t>(k)];
+  }
+  out->foot = foot;
+  out->eb = eb;
+  return true;
+}
+
+int64_t env_i64(const char* name, int64_t dflt) {
+  const char* v = std::getenv(name);
+  return v && std::atoll(v) > 0 ? std::atoll(v) : dflt;
+}
+
+bool pick_pipe(const Problem& p, HostPipe* out) {
+  const int r = p.rank();
+  const int64_t kmax = env_i64("TTB_HOST_SLABS", 12);
+  const int64_t min_row = env_i64("TTB_HOST_MIN_ROW", 4096);       // bytes
+  const int64_t min_slab = env_i64("TTB_HOST_MIN_SLAB_KB", 4096) << 10;
+  const int ea = kind_bytes(p.kind_a), eb = kind_bytes(p.kind_b);
+  const int64_t bytes = p.footprint_a() * ea + p.footprint_b() * eb;
+  const int64_t kwant = std::min(kmax, bytes / std::max<int64_t>(1, min_slab));
+  if (kwant < 2) return false;
+  const std::vector<int64_t> nb = p.b_extents();
+  bool found = false;
+  int64_t best_k = 0, best_w = 0;
+  for (int a = 0; a < r; ++a) {
+    const int64_t n = p.sizes[static_cast<size_t>(a)];
+    const int64_t k = std::min(n, kwant);
+    if (k < 2) continue;
+    const int64_t ext = (n + k - 1) / k;
+    HostPipe h;
+    const int q = p.perm[static_cast<size_t>(a)] - 1;
+    if (!slab_side(p.sizes, p.lda, a, ea, p.footprint_a(), &h.a) ||
+        !slab_side(nb, p.ldb, q, eb, p.footprint_b(), &h.b))
+      continue;
+    const int64_t wa = h.a.height == 1 ? INT64_MAX : ext * h.a.stride * ea;
+    const int64_t wb = h.b.height == 1 ? INT64_MAX : ext * h.b.stride * eb;
+    const int64_t w = std::min(wa, wb);
+    if (w < min_row) continue;
+    if (found && (k < best_k || (k == best_k && w <= best_w))) continue;
+    found = true;
+    best_k = k;
+    best_w = w;
+    h.axis = a;
+    h.n = n;
+    h.ext = ext;
+    h.b_in = p.beta != 0.0;
+    for (int j = 0; j < q; ++j)
+      if (p.ldb[static_cast<size_t>(j)] != nb[static_cast<size_t>(j)]) h.b_in = true;
+    *out = h;
+  }
+  return found;
+}
+
+// rows [j0, j1) of the slab axis on one side, host <-> device, same layout
+cudaError_t copy_slab(const SlabSide& sd, int64_t j0, int64_t j1, char* dst, const char* src,
+                      cudaMemcpyKind kind, cudaStream_t s) {
+  const int64_t w = (j1 - j0) * sd.stride;  // elements per row
+  const int64_t base = j0 * sd.stride;
+  int64_t h = sd.height;
+  // the last row may run past the buffer's end (padding of the lower axes)
+  const int64_t last = base + (h - 1) * sd.pitch;
+  const int64_t tail = std::min(w, sd.foot - last);
+  if (tail < w) --h;
+  const size_t e = static_cast<size_t>(sd.eb);
+  cudaError_t err = cudaSuccess;
+  for (int64_t h0 = 0; h0 < h && err == cudaSuccess; h0 += 32768) {
+    const int64_t hh = std::min<int64_t>(32768, h - h0);
+    const size_t off = static_cast<size_t>(base + h0 * sd.pitch) * e;
+    err = hh == 1 ? cudaMemcpyAsync(dst + off, src + off, static_cast<size_t>(w) * e, kind, s)
+                  : cudaMemcpy2DAsync(dst + off, static_cast<size_t>(sd.pitch) * e, src + off,
+                                      static_cast<size_t>(sd.pitch) * e, static_cast<size_t>(w) * e,
+                                      static_cast<size_t>(hh), kind, s);
+  }
+  if (err == cudaSuccess && tail < w) {
+    const size_t off = static_cast<size_t>(last) * e;
+    err = cudaMemcpyAsync(dst + off, src + off, static_cast<size_t>(tail) * e, kind, s);
+  }
+  return err;
+}
+
+int run_pipe(ttb_plan_s* plan, const HostPipe& hp, const void* A_host, void* B_host) {
+  cudaError_t e;
+  for (cudaStream_t* st : {&plan->ks, &plan->ds})
+    if (!*st && (e = cudaStreamCreateWithFlags(st, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamCreate");
+  const int64_t k = (hp.n + hp.ext - 1) / hp.ext;
+  while (static_cast<int64_t>(plan->evs.size()) < 2 * k) {
+    cudaEvent_t ev;
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_fail(e, "cudaEventCreate");
+    plan->evs.push_back(ev);
+  }
+  const Problem& mp = plan->merged.p;
+  char* dA = static_cast<char*>(plan->dA);
+  char* dB = static_cast<char*>(plan->dB);
+  const char* hA = static_cast<const char*>(A_host);
+  char* hB = static_cast<char*>(B_host);
+  for (int64_t i = 0; i < k; ++i) {
+    const int64_t j0 = i * hp.ext, j1 = std::min(hp.n, j0 + hp.ext), ext = j1 - j0;
+    cudaEvent_t ev_in = plan->evs[static_cast<size_t>(2 * i)];
+    cudaEvent_t ev_k = plan->evs[static_cast<size_t>(2 * i + 1)];
+    if ((e = copy_slab(hp.a, j0, j1, dA, hA, cudaMemcpyHostToDevice, plan->hs)) != cudaSuccess)
+      return cuda_fail(e, "H2D A slab");
+    if (hp.b_in && (e = copy_slab(hp.b, j0, j1, dB, hB, cudaMemcpyHostToDevice, plan->hs)) != cudaSuccess)
+      return cuda_fail(e, "H2D B slab");
+    cudaEventRecord(ev_in, plan->hs);
+    cudaStreamWaitEvent(plan->ks, ev_in, 0);
+    std::unique_ptr<ttb_plan_s>& sub = plan->chunk_plans[ext];
+    if (!sub) {  // the slab's problem: same perm/lda/ldb, slab axis extent = ext
+      Problem q = mp;
+      q.sizes[static_cast<size_t>(hp.axis)] = ext;
+      const int rc = build_plan(q, TTB_PLAN_NO_CACHE, &sub);
+      if (rc) return rc;
+      std::string why;
+      Prepared pr;  // keep the parent's (possibly autotuned) variant where it applies
+      if (prepare(sub->geo, plan->prep.spec, sub->sms, &pr, &why)) sub->prep = pr;
+    }
+    const int rc = execute(sub.get(), sub->prep, dA + static_cast<size_t>(j0 * hp.a.stride) * hp.a.eb,
+                           dB + static_cast<size_t>(j0 * hp.b.stride) * hp.b.eb, plan->ks, mp.alpha,
+                           mp.beta);
+    if (rc) return rc;
+    cudaEventRecord(ev_k, plan->ks);
+    cudaStreamWaitEvent(plan->ds, ev_k, 0);
+    if ((e = copy_slab(hp.b, j0, j1, hB, dB, cudaMemcpyDeviceToHost, plan->ds)) != cudaSuccess)
+      return cuda_fail(e, "D2H B slab");
+  }
+  if ((e = cudaStreamSynchronize(plan->ds)) != cudaSuccess) return cuda_fail(e, "sync");
+  return ok();
 }
 
 }  // namespace
@@ -349,12 +528,17 @@ int ttb_plan_execute_host(ttb_plan plan, const void* A_host, void* B_host) {
     if (!A_host || !B_host) return fail(TTB_EINVAL, "host buffers: null pointer");
     cudaError_t e;
     const size_t na = plan->bytes_a(), nb = plan->bytes_b();
-    if (!plan->dA) {
-      if ((e = cudaMalloc(&plan->dA, na)) != cudaSuccess) return cuda_fail(e, "cudaMalloc A");
-      if ((e = cudaMalloc(&plan->dB, nb)) != cudaSuccess) return cuda_fail(e, "cudaMalloc B");
-      if ((e = cudaStreamCreateWithFlags(&plan->hs, cudaStreamNonBlocking)) != cudaSuccess)
-        return cuda_fail(e, "cudaStreamCreate");
+    if (!plan->hs && (e = cudaStreamCreateWithFlags(&plan->hs, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamCreate");
+    if (!plan->dA && (e = cudaMalloc(&plan->dA, na)) != cudaSuccess) return cuda_fail(e, "cudaMalloc A");
+
+    if (!plan->dB && (e = cudaMalloc(&plan->dB, nb)) != cudaSuccess) return cuda_fail(e, "cudaMalloc B");
+    const char* hp = std::getenv("TTB_HOST_PATH");  // "staged": force the sequential path
+    if (!(hp && std::strcmp(hp, "staged") == 0) && pinned(A_host) && pinned(B_host)) {
+      HostPipe hpipe;
+      if (pick_pipe(plan->merged.p, &hpipe)) return run_pipe(plan, hpipe, A_host, B_host);
     }
+
     cudaStream_t s = plan->hs;
     // B's padding must come back unchanged, so B travels to the device when
     // it is read (beta != 0) or padded

@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$? >> gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --no-cpu > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 300 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "host" > gpurun_out/pytest_host.log 2>&1; echo rc=$? >> gpurun_out/pytest_host.log
+timeout 600 python scripts/e2e_probe.py > gpurun_out/e2e_probe.log 2>&1; echo rc=$? >> gpurun_out/e2e_probe.log

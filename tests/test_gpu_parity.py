@@ -267,6 +267,34 @@ def test_host_end_to_end_path(coracle):
         assert got.tobytes() == want.tobytes()
 
 
+def test_host_pinned_overlapped_path(coracle, monkeypatch):
+    """Pinned host buffers take the slab pipeline (H2D of slab i+1 overlapping
+    the kernel and the D2H of slab i); the thresholds are lowered so these
+    small problems cut into several slabs, padded rows and clipped tails
+    included.  The second pass per problem reuses the slab plans."""
+    monkeypatch.setenv("TTB_HOST_MIN_SLAB_KB", "1")
+    monkeypatch.setenv("TTB_HOST_MIN_ROW", "4")
+    rng = np.random.default_rng(9)
+    for kind, perm, sizes, lda, ldb, beta in [
+            ("d", [2, 1], [300, 200], None, None, 0.0),
+            ("s", [3, 1, 2], [37, 50, 61], [40, 50, 70], [50, 80, 37], 0.0),
+            ("c", [2, 3, 1], [33, 20, 70], None, None, 1.5),
+            ("s", [1, 2], [1000, 77], [1003, 77], None, 0.0),
+            ("z", [4, 3, 2, 1], [9, 10, 11, 120], None, None, -1.0),
+            ("d", [2, 1, 3], [31, 17, 9], [33, 17, 9], [19, 31, 10], 0.0),
+            ("s", [1, 3, 2], [8, 60, 50], [9, 60, 50], [8, 55, 61], 2.0)]:
+        A, B = _inputs(coracle, rng, kind, kind, perm, sizes, lda, ldb, beta)
+        want = B.copy()
+        coracle.transpose(kind, kind, perm, sizes, lda, ldb, 0.5, A, beta, want)
+        plan = ttb.GpuPlan(ttb.make_problem(perm, sizes, kind, kind, 0.5, beta, lda, ldb))
+        ha = torch.from_numpy(A.view(np.uint8).copy()).pin_memory()
+        hb = torch.from_numpy(B.view(np.uint8).copy()).pin_memory()
+        for _ in range(2):  # the second pass reuses the chunk plans
+            hb.copy_(torch.from_numpy(B.view(np.uint8).copy()))
+            plan.execute_host(ha, hb)
+            assert hb.numpy().tobytes() == want.tobytes(), (kind, perm, sizes)
+
+
 def test_kernels_actually_launch():
     before = ttb.launch_count()
     p = ttb.make_problem([2, 1], [64, 64])

@@ -264,7 +264,7 @@ int64_t env_i64(const char* name, int64_t dflt) {
 
 bool pick_pipe(const Problem& p, HostPipe* out) {
   const int r = p.rank();
-  const int64_t kmax = env_i64("TTB_HOST_SLABS", 12);
+  const int64_t kmax = env_i64("TTB_HOST_SLABS", 32);
   const int64_t min_row = env_i64("TTB_HOST_MIN_ROW", 4096);       // bytes
   const int64_t min_slab = env_i64("TTB_HOST_MIN_SLAB_KB", 4096) << 10;
   const int ea = kind_bytes(p.kind_a), eb = kind_bytes(p.kind_b);

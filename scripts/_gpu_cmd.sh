@@ -1,2 +1,2 @@
-timeout 300 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "host" > gpurun_out/pytest_host.log 2>&1; echo rc=$? >> gpurun_out/pytest_host.log
-timeout 600 python scripts/e2e_probe.py > gpurun_out/e2e_probe.log 2>&1; echo rc=$? >> gpurun_out/e2e_probe.log
+timeout 600 python bench.py > gpurun_out/bench_full.log 2>&1; echo rc=$? >> gpurun_out/bench_full.log
+timeout 300 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo rc=$? >> gpurun_out/bench_ref.log

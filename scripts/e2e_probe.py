@@ -45,7 +45,7 @@ def row(name):
     hb = torch.empty(nb * sz, dtype=torch.uint8, pin_memory=True)
     plan = ttb.GpuPlan(q)
     res = {}
-    for path in ("staged", "overlap"):
+    for path in os.environ.get("PROBE_PATHS", "staged,overlap").split(","):
         os.environ["TTB_HOST_PATH"] = path
         plan.execute_host(ha, hb)
         t0 = time.perf_counter()
@@ -56,6 +56,7 @@ def row(name):
 
 
 if __name__ == "__main__":
-    pcie_ceilings()
+    if not os.environ.get("PROBE_NO_PCIE"):
+        pcie_ceilings()
     for n in sys.argv[1:] or [f"c5_t{t:02d}" for t in range(24)]:
         row(n)

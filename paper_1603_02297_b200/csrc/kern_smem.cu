@@ -50,7 +50,9 @@ cudaError_t with_smem(int ka, int kb, int mode, int dense, int kk, F&& f) {
   });
 }
 
-int carveout() {
+}  // namespace
+
+int smem_carveout() {
   // shared/L1 split of the unified array (percent shared).  Half leaves L1 room
   // for the cp.async (.ca) line allocations; TTB_CARVEOUT overrides, < 0 keeps
   // the driver default.
@@ -60,10 +62,10 @@ int carveout() {
   }();
   return c;
 }
-}  // namespace
 
 cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                         cudaStream_t s) {
+  if (p.dense == 4) return launch_vtile(ka, kb, mode, p, l, s);
   return with_smem(ka, kb, mode, p.dense, p.ept, [&](auto fn) {
     if (l.smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
@@ -78,8 +80,8 @@ cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Lau
 int occupancy_smem(int ka, int kb, int mode, int dense, int ept, int block, int smem) {
   int n = 0;
   with_smem(ka, kb, mode, dense, ept, [&](auto fn) {
-    if (carveout() >= 0)
-      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout());
+    if (smem_carveout() >= 0)
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, smem_carveout());
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem);
   });

@@ -21,6 +21,11 @@ cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Lau
 int occupancy_copy(int ka, int kb, int v, int mode, bool long_rows, int block);
 int occupancy_rt(int ka, int kb, int mx, int my, int mode, int block);
 int occupancy_smem(int ka, int kb, int mode, int dense, int ept, int block, int smem);
+// vtile_kernel (SmemParams::dense == 4), kern_vtile.cu
+cudaError_t launch_vtile(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
+                         cudaStream_t s);
+int occupancy_vtile(int ka, int kb, int mode, int va, int vb, int block, int smem);
+int smem_carveout();
 
 // data utilities (util.cu)
 struct BoxParams {

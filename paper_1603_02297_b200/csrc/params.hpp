@@ -111,9 +111,10 @@ struct SmemParams {
   uint32_t items;
   // dense fast path: S == 1, X contiguous in A, Y contiguous in B, tx/ty powers
   // of two -> the walks need shifts and masks only, no per-element division
-  int dense;              // 0 generic, 1 dense (any tile), 2 dense power-of-two tile
+  int dense;              // 0 generic, 1 dense (any tile), 2/3 dense power-of-two tile, 4 vector tile
   uint32_t ltx, lty;
   int ept;                // dense with tx,ty <= 256 and tx*ty = 256*ept: fixed walks
+  int va, vb;             // dense == 4 (vtile_kernel): vector widths along x in A / y in B
 };
 
 // Launch shape chosen by the planner.

@@ -162,6 +162,56 @@ uint32_t best_row_length(uint32_t S, uint32_t tx, uint32_t ty, int ebytes) {
   return best;
 }
 
+bool x_dense_in_a(const Geo& g, const std::vector<int>& xs);
+bool y_dense_in_b(const Geo& g, const std::vector<int>& ys);
+
+// vector widths of vtile_kernel for a tile (false: element-wise only)
+bool vtile_widths(const Geo& g, const std::vector<int>& xs, const std::vector<int>& ys, int64_t tx,
+                  int64_t ty, int* va, int* vb) {
+  if (g.ka != g.kb || g.ka > 2 || !x_dense_in_a(g, xs) || !y_dense_in_b(g, ys)) return false;
+  auto width = [&](const std::vector<int>& grp, const int64_t* st, int64_t t, int e) {
+    for (int v = std::min(4, 16 / e); v > 1; v /= 2) {
+      if (t % v || t / v > 256) continue;
+      bool ok = true;
+      for (int a = 0; a < g.r && ok; ++a)
+        if (std::find(grp.begin(), grp.end(), a) == grp.end() && st[a] % v) ok = false;
+      if (ok) return v;
+    }
+    return 1;
+  };
+  *va = width(xs, g.sa, tx, g.eA);
+  *vb = width(ys, g.sb, ty, g.eB);
+  return *va * *vb > 1;
+}
+
+// row pitch of vtile_kernel's A tile: a multiple of VA (16-byte chunk
+// destinations) with the fewest shared-memory wavefronts for the store walk
+// (lane t reads rows yl..yl+VB-1 of column c0, yl = (t % (ty/VB))*VB, c0 = t / (ty/VB))
+uint32_t vtile_row_length(uint32_t tx, uint32_t ty, int va, int vb, int ebytes) {
+  const int words = std::max(1, ebytes / 4);
+  const int phase = std::max(1, 32 / words);  // lanes per shared-memory wavefront at best
+  const uint32_t lcv = ty / vb;
+  uint32_t base = (tx + va - 1) / va * va, best = base;
+  int best_w = 1 << 30;
+  for (uint32_t rl = base; rl < base + 32; rl += va) {
+    int wf = 0;
+    for (int p0 = 0; p0 < 32; p0 += phase) {
+      int cnt[32] = {};
+      for (int t = p0; t < p0 + phase; ++t) {
+        const uint32_t c0 = t / lcv, yl = (t % lcv) * vb;
+        const uint32_t w0 = (yl * rl + c0) * words;
+        for (int q = 0; q < words; ++q) ++cnt[(w0 + q) % 32];
+      }
+      wf += *std::max_element(cnt, cnt + 32);
+    }
+    if (wf < best_w) {
+      best_w = wf;
+      best = rl;
+    }
+  }
+  return best;
+}
+
 int64_t pow2_ceil(int64_t v) {
   int64_t p = 1;
   while (p < v) p *= 2;
@@ -259,6 +309,21 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
                    [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
   for (size_t i = 0; i < cand.size() && i < 8; ++i) {
     out->push_back(cand[i]);
+    int va, vb;
+    if (!shared && vtile_widths(g, x_group(0, cand[i].kx), y_group(g, 0, cand[i].ky),
+                                std::min<int64_t>(cand[i].tx, prod(g, x_group(0, cand[i].kx))),
+                                std::min<int64_t>(cand[i].ty, prod(g, y_group(g, 0, cand[i].ky))),
+                                &va, &vb)) {
+      // the element-wise kernels for the same tile (and B-direct form)
+      Spec e = cand[i];
+      e.vec = 0;
+      e.cost += 0.03;
+      out->push_back(e);
+      if (g.mode == 2) {
+        e.bp = 0;
+        out->push_back(e);
+      }
+    }
     if (g.mode == 2) {  // beta != 0: also try B read directly (smaller stages, more CTAs)
       Spec d = cand[i];
       d.bp = 0;
@@ -318,8 +383,9 @@ std::string Spec::text() const {
                     w2, lx, kx, ky, order, occ);
       break;
     default:
-      std::snprintf(buf, sizeof buf, "kern=smem;kx=%d;ky=%d;tx=%d;ty=%d;order=%d;occ=%d;st=%d;bp=%d",
-                    kx, ky, tx, ty, order, occ, st, bp);
+      std::snprintf(buf, sizeof buf,
+                    "kern=smem;kx=%d;ky=%d;tx=%d;ty=%d;order=%d;occ=%d;st=%d;bp=%d;vec=%d", kx, ky, tx,
+                    ty, order, occ, st, bp, vec);
   }
   return buf;
 }
@@ -371,6 +437,8 @@ bool Spec::parse(const std::string& s, Spec* out) {
       p.st = static_cast<int>(x);
     else if (k == "bp")
       p.bp = static_cast<int>(x);
+    else if (k == "vec")
+      p.vec = static_cast<int>(x);
     else
       return false;
   }
@@ -499,9 +567,10 @@ std::vector<Spec> candidates(const Geo& g) {
   for (const Spec& s : out)
     if (!have_fb && (s.v == kSmem || (s.v == kCopy && s.w1 == 1))) {
       fallback = s;
+      fallback.vec = 0;
       have_fb = true;
     }
-  if (out.size() > 24) out.resize(24);
+  if (out.size() > 32) out.resize(32);
   if (have_fb) out.push_back(fallback);
   return out;
 }
@@ -638,6 +707,17 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
       }
     }
     m.rl = best_row_length(m.S, m.tx, m.ty, g.eA);
+    m.va = m.vb = 1;
+    // vector tile: every A tile row starts on a VA boundary, every B tile
+    // column on a VB boundary (vtile.cuh); equal kinds s/d/c, two stages
+    int va = 1, vb = 1;
+    if (s.vec && s.st == 2 && small && m.S == 1 && vtile_widths(g, xs, ys, m.tx, m.ty, &va, &vb)) {
+      m.dense = 4;
+      m.ept = 0;
+      m.va = va;
+      m.vb = vb;
+      m.rl = vtile_row_length(m.tx, m.ty, va, vb, g.eA);
+    }
     m.dS = Div32::make(m.S);
     m.dtx = Div32::make(m.tx);
     m.dty = Div32::make(m.ty);
@@ -660,11 +740,13 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
                 : static_cast<int64_t>(m.tx + m.ty) * 2 * 8 + static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);
-    const int occ = std::min(occ_cap, std::max(1, occupancy_smem(g.ka, g.kb, p.mode, m.dense,
-                                                                 m.ept, 256, p.l.smem)));
+    const int occ = std::min(
+        occ_cap, std::max(1, m.dense == 4 ? occupancy_vtile(g.ka, g.kb, p.mode, m.va, m.vb, 256, p.l.smem)
+                                          : occupancy_smem(g.ka, g.kb, p.mode, m.dense, m.ept, 256,
+                                                           p.l.smem)));
     p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(m.items, int64_t{occ} * sms)));
-    p.a_align = std::min(16, g.eA);  // whole elements (Vec<SA, C>) move as a unit
-    p.b_align = std::min(16, g.eB);
+    p.a_align = std::min(16, g.eA * m.va);  // whole elements (Vec<SA, C>) / vectors move as a unit
+    p.b_align = std::min(16, g.eB * m.vb);
   }
   p.l.block = 256;
   *out = p;

@@ -42,6 +42,7 @@ struct Spec {
   int occ = 0;         // CTAs per SM (0: occupancy limit)
   int st = 2;          // smem: cp.async pipeline stages (dense tiles: 2 or 3)
   int bp = 1;          // smem, beta != 0: B through the cp.async ring (1) or direct (0)
+  int vec = 1;         // smem: vector tile kernel where the strides allow it (0: element-wise)
   double cost = 0;     // heuristic rank (lower first)
 
   std::string text() const;

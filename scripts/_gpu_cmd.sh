@@ -1,2 +1,1 @@
-timeout 600 python bench.py > gpurun_out/bench_full.log 2>&1; echo rc=$? >> gpurun_out/bench_full.log
-timeout 300 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo rc=$? >> gpurun_out/bench_ref.log
+for c in c5_t20 c5_t02 c5_t18; do timeout 200 python scripts/run_case.py $c --iters 5 --check --top 14; done > gpurun_out/cases.log 2>&1

@@ -159,6 +159,50 @@ def test_sweep_rows_match_reference_checksums():
         torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("kind", ["s", "d", "c"])
+def test_vector_tile_shapes(coracle, kind):
+    """vtile_kernel (vector cp.async rows / vector column stores): shapes whose
+    strides admit vectors on one or both sides, ragged tile edges (partial
+    zero-filled chunks, element-wise column tails), padding, every mode; every
+    candidate plan is run and at least one of them must be a vector tile."""
+    rng = np.random.default_rng(40 + kind_id(kind))
+    cases = [
+        ([2, 1], [64, 48], None, None),
+        ([2, 1], [84, 36], None, None),
+        ([2, 1], [130, 70], None, None),            # partial chunks and column tails
+        ([2, 1], [37, 44], [40, 44], [44, 40]),     # padded, odd extent
+        ([3, 1, 2], [20, 12, 9], None, None),
+        ([2, 3, 1], [36, 5, 10], None, None),
+        ([5, 2, 4, 1, 3], [10, 8, 3, 36, 2], None, None),
+        ([4, 3, 1, 2], [12, 9, 4, 14], [12, 10, 4, 14], [4, 15, 9, 12]),
+    ]
+    seen = 0
+    for perm, sizes, lda, ldb in cases:
+        for alpha, beta in [(1.0, 0.0), (1.5, 0.0), (0.5, -2.0)]:
+            A, B = _inputs(coracle, rng, kind, kind, perm, sizes, lda, ldb, beta)
+            want = B.copy()
+            coracle.transpose(kind, kind, perm, sizes, lda, ldb, alpha, A, beta, want)
+            p = ttb.make_problem(perm, sizes, kind, kind, alpha, beta, lda, ldb)
+            for text in all_plans(kind, kind, perm, sizes, lda, ldb, alpha, beta):
+                plan = ttb.GpuPlan(p, cache=False)
+                plan.select(text)
+                seen += plan.describe().endswith("fn=vtile")
+                got = run_gpu(kind, kind, perm, sizes, lda, ldb, alpha, A, beta, B, plan_text=text)
+                assert got.tobytes() == want.tobytes(), (perm, sizes, alpha, beta, text)
+            # explicit vector tiles (tile sides that are multiples of the vector width)
+            for tx, ty in [(16, 12), (20, 8), (32, 32), (12, 36)]:
+                text = f"kern=smem;kx=1;ky=1;tx={tx};ty={ty};order=0;occ=0;st=2;bp={int(beta != 0)};vec=1"
+                plan = ttb.GpuPlan(p, cache=False)
+                try:
+                    plan.select(text)
+                except ValueError:
+                    continue
+                seen += plan.describe().endswith("fn=vtile")
+                got = run_gpu(kind, kind, perm, sizes, lda, ldb, alpha, A, beta, B, plan_text=text)
+                assert got.tobytes() == want.tobytes(), (perm, sizes, alpha, beta, text)
+    assert seen > 0
+
+
 def test_edge_cases(coracle):
     rng = np.random.default_rng(3)
     cases = [

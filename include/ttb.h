@@ -141,10 +141,14 @@ int ttb_plan_destroy(ttb_plan plan);
 int ttb_plan_execute(ttb_plan plan, const void* A, void* B, ttb_stream stream);
 
 /* End-to-end call on HOST buffers: host->device copy of A (and of B when
- * beta != 0), the kernel, device->host copy of B, pipelined in chunks on
- * plan-owned device buffers.  Synchronous; returns when B_host is written.
- * Host buffers should be pinned (cudaHostAlloc / cudaHostRegister) for
- * full PCIe bandwidth. */
+ * beta != 0 or padded), the kernel, device->host copy of B, on plan-owned
+ * device buffers.  Synchronous; returns when B_host is written.  With both
+ * buffers pinned (cudaHostAlloc / cudaHostRegister) the problem is cut into
+ * slabs along one merged axis and the slabs are pipelined: slab i+1 streams in
+ * while slab i's kernel runs and its B part streams out (PCIe is full duplex);
+ * pageable buffers take the sequential path.  Env overrides (tuning/tests):
+ * TTB_HOST_SLABS (max slabs, 32), TTB_HOST_MIN_ROW (bytes per 2D-copy row,
+ * 4096), TTB_HOST_MIN_SLAB_KB (4096), TTB_HOST_PATH=staged. */
 int ttb_plan_execute_host(ttb_plan plan, const void* A_host, void* B_host);
 
 /* Measured autotune: time every candidate variant of the plan on the given
@@ -164,6 +168,39 @@ int ttb_plan_candidates(ttb_plan plan, char* buf, size_t len);
 int ttb_plan_select(ttb_plan plan, const char* plan_text);
 /* per-launch: number of kernel launches and the kernel names of one execute */
 int ttb_plan_launches(ttb_plan plan, int* launches_per_execute);
+
+/* ------------------------------------------ persistent solution cache -- */
+
+/* The reference's SolutionCache (tuner.cpp:81-205) as a native file store:
+ * one tab-separated line per entry, "problem_key \t hardware_key \t plan \t
+ * bandwidth_gibs \t ISO-8601 UTC timestamp", appended under an exclusive
+ * flock; lookup reads under a shared flock, skips malformed lines (warning on
+ * stderr) and returns the LAST entry matching both keys.  Bandwidth is GiB/s
+ * (2^30), as the reference stores it. */
+int ttb_cache_store(const char* file, const char* problem_key, const char* hardware_key,
+                    const char* plan_text, double bandwidth_gibs);
+/* *found = 0/1; plan text into plan_buf; bandwidth / timestamp optional (NULL) */
+int ttb_cache_lookup(const char* file, const char* problem_key, const char* hardware_key,
+                     char* plan_buf, size_t plan_len, double* bandwidth_gibs, char* ts_buf,
+                     size_t ts_len, int* found);
+/* this GPU: "<device name>:sm<major><minor>:<SMs>sms:ttb<version>" (the
+ * reference keys hardware by host/threads/micro-width, default_hardware_key) */
+int ttb_hardware_key(char* buf, size_t len);
+/* pipeline.cpp:102-185 for one plan: look the plan up by (canonical_key of
+ * the original problem, hardware key); on a hit select it, on a miss (or a
+ * stale entry that no longer applies) autotune on A/B and store the winner.
+ * *hit = 1 on a cache hit.  B ends holding one application, as autotune. */
+int ttb_plan_tune_cached(ttb_plan plan, const char* cache_file, const void* A, void* B,
+                         int warmups, int reps, ttb_stream stream, int* hit);
+
+/* ------------------------------------------ the paper's benchmark suite -- */
+
+/* build_benchmark (benchmark.cpp:166-220): the 57 synthetic cases (19
+ * non-mergeable perms over d = 2..6 times balanced / skewA / skewB extents of
+ * ~volume_bytes, alpha = beta = 1), drawn with mt19937_64(seed).  Writes the
+ * manifest, one benchmark_case_line per case ("case=...;perm=...;size=...;
+ * kinds=..;alpha=..;beta=..;category=..;config=.."), '\n'-separated. */
+int ttb_benchmark_manifest(int64_t volume_bytes, int kind, uint64_t seed, char* buf, size_t len);
 
 /* ------------------------------------------- multi-GPU partitioning -- */
 

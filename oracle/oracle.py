@@ -182,6 +182,33 @@ class RefOracle:
         L.ref_session_run.restype = C.c_double
         L.ref_session_tune.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p,
                                        C.c_size_t, C.POINTER(C.c_double)]
+        L.ref_benchmark_manifest.argtypes = [C.c_int64, C.c_int, C.c_uint64, C.c_char_p,
+                                             C.c_size_t]
+        L.ref_cache_store.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_double,
+                                      C.c_char_p]
+        L.ref_cache_lookup.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_size_t,
+                                       C.POINTER(C.c_double), _i32p]
+
+    def benchmark_manifest(self, volume_bytes: int, kind, seed: int):
+        """build_benchmark + write_benchmark_manifest of the reference."""
+        out = C.create_string_buffer(1 << 16)
+        if self.lib.ref_benchmark_manifest(volume_bytes, kind_id(kind), seed, out, 1 << 16):
+            raise ValueError("reference build_benchmark failed")
+        return [l for l in out.value.decode().split("\n") if l]
+
+    def cache_store(self, file, pkey, hkey, plan, gibs, ts="2026-01-01T00:00:00Z"):
+        if self.lib.ref_cache_store(str(file).encode(), pkey.encode(), hkey.encode(),
+                                    plan.encode(), gibs, ts.encode()):
+            raise ValueError("reference SolutionCache::store failed")
+
+    def cache_lookup(self, file, pkey, hkey):
+        out = C.create_string_buffer(1024)
+        gibs = C.c_double(0)
+        found = C.c_int(0)
+        if self.lib.ref_cache_lookup(str(file).encode(), pkey.encode(), hkey.encode(), out, 1024,
+                                     C.byref(gibs), C.byref(found)):
+            raise ValueError("reference SolutionCache::lookup failed")
+        return (out.value.decode(), gibs.value) if found.value else None
 
     def validate(self, perm, sizes, lda=None, ldb=None, kind_a="s", kind_b="s") -> Optional[str]:
         msg = C.create_string_buffer(512)

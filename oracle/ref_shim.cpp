@@ -13,11 +13,13 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "support.hpp"
+#include "ttune/benchmark.hpp"
 #include "ttune/executor.hpp"
 #include "ttune/problem.hpp"
 #include "ttune/search.hpp"
@@ -212,6 +214,40 @@ int ref_session_tune(void* h, int threads, int max_impl, int warmups, int reps, 
     const TuneResult r = tune(n, q, TimingProtocol{warmups, reps, threads});
     put(plan_out, len, r.records[r.best].plan.serialize());
     if (gibs) *gibs = r.records[r.best].bandwidth_gibs;
+  });
+}
+
+// the reference's benchmark suite manifest (benchmark.cpp:166-220, 258-270)
+int ref_benchmark_manifest(std::int64_t volume_bytes, int kind, std::uint64_t seed, char* out,
+                           std::size_t len) {
+  return guarded(nullptr, 0, [&] {
+    const ElementKind k[] = {ElementKind::real32, ElementKind::real64, ElementKind::complex64,
+                             ElementKind::complex128};
+    std::ostringstream os;
+    write_benchmark_manifest(os, build_benchmark(volume_bytes, k[kind], seed));
+    put(out, len, os.str());
+  });
+}
+
+// the reference's SolutionCache: store one entry / look one up (tuner.cpp:81-205)
+int ref_cache_store(const char* file, const char* pkey, const char* hkey, const char* plan,
+                    double gibs, const char* ts) {
+  return guarded(nullptr, 0, [&] {
+    SolutionCache c(file);
+    c.store(SolutionEntry{pkey, hkey, CandidatePlan::parse(plan), gibs, ts});
+  });
+}
+
+int ref_cache_lookup(const char* file, const char* pkey, const char* hkey, char* plan_out,
+                     std::size_t len, double* gibs, int* found) {
+  return guarded(nullptr, 0, [&] {
+    SolutionCache c(file);
+    const auto e = c.lookup(pkey, hkey);
+    *found = e ? 1 : 0;
+    if (e) {
+      put(plan_out, len, e->plan.serialize());
+      *gibs = e->bandwidth_gibs;
+    }
   });
 }
 

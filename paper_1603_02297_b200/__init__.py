@@ -29,6 +29,8 @@ __all__ = [
     "canonical_key", "merge_indices", "TensorBuffer", "make_buffer_a", "make_buffer_b",
     "reference_transpose", "execute_plan", "GpuPlan", "bandwidth_gbs", "shard_boxes",
     "fill_uniform", "fill_sentinel", "checksum", "launch_count", "TTBError", "version",
+    "SolutionEntry", "SolutionCache", "hardware_key", "BenchmarkCase", "build_benchmark",
+    "benchmark_case_line",
 ]
 
 
@@ -243,6 +245,92 @@ def launch_count() -> int:
     return int(lib.ttb_launch_count())
 
 
+# ------------------------------------------------- persistent solutions --
+
+@dataclass
+class SolutionEntry:
+    """tuner.hpp:45-51: one line of the solution file (bandwidth in GiB/s)."""
+    problem_key: str
+    hardware_key: str
+    plan: str
+    bandwidth_gibs: float
+    timestamp: str = ""
+
+
+class SolutionCache:
+    """The reference's SolutionCache (tuner.cpp:81-205) backed by the native
+    store: tab-separated lines under flock, last matching entry wins."""
+
+    def __init__(self, file):
+        self.file = str(file)
+
+    def lookup(self, problem_key: str, hardware_key: str) -> Optional[SolutionEntry]:
+        plan = C.create_string_buffer(1024)
+        ts = C.create_string_buffer(64)
+        bw = C.c_double(0.0)
+        found = C.c_int(0)
+        check(lib.ttb_cache_lookup(self.file.encode(), problem_key.encode(),
+                                   hardware_key.encode(), plan, 1024, C.byref(bw), ts, 64,
+                                   C.byref(found)))
+        if not found.value:
+            return None
+        return SolutionEntry(problem_key, hardware_key, plan.value.decode(), bw.value,
+                             ts.value.decode())
+
+    def store(self, entry: SolutionEntry) -> None:
+        check(lib.ttb_cache_store(self.file.encode(), entry.problem_key.encode(),
+                                  entry.hardware_key.encode(), entry.plan.encode(),
+                                  float(entry.bandwidth_gibs)))
+
+
+def hardware_key() -> str:
+    """"<device>:sm<cc>:<SMs>sms:ttb<version>" of the current CUDA device."""
+    buf = C.create_string_buffer(512)
+    check(lib.ttb_hardware_key(buf, 512))
+    return buf.value.decode()
+
+
+# ------------------------------------------------------- benchmark suite --
+
+@dataclass
+class BenchmarkCase:
+    """benchmark.hpp:17-22."""
+    id: str
+    problem: "TransposeProblem"
+    category: str
+    config: str
+
+
+def _manifest(volume_bytes: int, kind, seed: int) -> List[str]:
+    k = ElementKind.from_code(kind) if isinstance(kind, str) else ElementKind(kind)
+    n = 1 << 16
+    buf = C.create_string_buffer(n)
+    check(lib.ttb_benchmark_manifest(int(volume_bytes), int(k.value), int(seed), buf, n))
+    return [l for l in buf.value.decode().split("\n") if l]
+
+
+def build_benchmark(volume_bytes: int, kind="s", seed: int = 42) -> List[BenchmarkCase]:
+    """benchmark.cpp:166-220: the paper's 57 cases (alpha = beta = 1)."""
+    cases = []
+    for line in _manifest(volume_bytes, kind, seed):
+        f = dict(kv.split("=", 1) for kv in line.split(";"))
+        perm = [int(x) for x in f["perm"].split(",")]
+        sizes = [int(x) for x in f["size"].split(",")]
+        p = make_problem(perm, sizes, f["kinds"][0], f["kinds"][1], float(f["alpha"]),
+                         float(f["beta"]))
+        cases.append(BenchmarkCase(f["case"], p, f["category"], f["config"]))
+    return cases
+
+
+def benchmark_case_line(case: BenchmarkCase) -> str:
+    """benchmark.cpp:258-266 -- the manifest line of a case."""
+    p = case.problem
+    kinds = p.kind_a.code + p.kind_b.code
+    return (f"case={case.id};perm={','.join(map(str, p.perm.map))};"
+            f"size={','.join(map(str, p.sizes))};kinds={kinds};alpha={p.alpha:.6g};"
+            f"beta={p.beta:.6g};category={case.category};config={case.config}")
+
+
 # ----------------------------------------------------------------- buffers --
 
 def _torch():
@@ -357,6 +445,19 @@ class GpuPlan:
         check(lib.ttb_plan_autotune(self._h, C.c_void_p(pa), C.c_void_p(pb), warmups, reps,
                                     _stream(stream)))
         return self.describe()
+
+    def tune_cached(self, a, b, cache_file: str, warmups: int = 2, reps: int = 3,
+                    stream=None) -> bool:
+        """pipeline.cpp:102-185 for this plan: select the cached plan of (canonical
+        key, hardware key) from `cache_file`, or autotune and append the winner.
+        Returns True on a cache hit.  B holds one application afterwards."""
+        pa = a.data_ptr() if hasattr(a, "data_ptr") else int(a)
+        pb = b.data_ptr() if hasattr(b, "data_ptr") else int(b)
+        hit = C.c_int(0)
+        check(lib.ttb_plan_tune_cached(self._h, str(cache_file).encode(), C.c_void_p(pa),
+                                       C.c_void_p(pb), warmups, reps, _stream(stream),
+                                       C.byref(hit)))
+        return bool(hit.value)
 
     def describe(self) -> str:
         buf = C.create_string_buffer(512)

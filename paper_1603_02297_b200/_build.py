@@ -83,14 +83,18 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
-def build_variant(name: str, defines: list) -> str:
-    """Experiment build: every source with extra -D flags into _lib/libttb_<name>.so
-    (load it with TTB_LIB_PATH; the product always uses libttb.so)."""
+def build_variant(name: str, defines: list, only=None) -> str:
+    """Experiment build: sources with extra -D flags into _lib/libttb_<name>.so
+    (load it with TTB_LIB_PATH; the product always uses libttb.so).  `only`:
+    recompile just these source basenames, the rest from the product objects."""
+    build()
     objdir = os.path.join(LIBDIR, f"obj_{name}")
     os.makedirs(objdir, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
     def one(src):
+        if only and os.path.basename(src) not in only:
+            return os.path.join(OBJDIR, os.path.basename(src) + ".o")
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [_nvcc(), *_flags(), *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         subprocess.run(cmd, check=True, capture_output=True)
@@ -105,6 +109,9 @@ def build_variant(name: str, defines: list) -> str:
 
 if __name__ == "__main__":
     if len(sys.argv) > 2 and sys.argv[1] == "--variant":
-        print(build_variant(sys.argv[2], sys.argv[3:]))
+        args = sys.argv[3:]
+        only = [a[len("--only="):] for a in args if a.startswith("--only=")]
+        print(build_variant(sys.argv[2], [a for a in args if not a.startswith("--only=")],
+                            only=only or None))
     else:
         print(build(verbose="--verbose" in sys.argv))

@@ -53,6 +53,12 @@ _SIGS = {
     "ttb_checksum": ([C.c_int, C.c_int, i64p, i64p, i64p, i64p, vp, C.POINTER(C.c_uint64), vp],
                      C.c_int),
     "ttb_launch_count": ([], C.c_uint64),
+    "ttb_cache_store": ([C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_double], C.c_int),
+    "ttb_cache_lookup": ([C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_size_t,
+                          C.POINTER(C.c_double), C.c_char_p, C.c_size_t, i32p], C.c_int),
+    "ttb_hardware_key": ([C.c_char_p, C.c_size_t], C.c_int),
+    "ttb_plan_tune_cached": ([vp, C.c_char_p, vp, vp, C.c_int, C.c_int, vp, i32p], C.c_int),
+    "ttb_benchmark_manifest": ([C.c_int64, C.c_int, C.c_uint64, C.c_char_p, C.c_size_t], C.c_int),
     "ttb_debug_candidates": ([C.c_int, C.c_int, C.c_int, i32p, i64p, i64p, i64p, C.c_double,
                               C.c_double, C.c_char_p, C.c_size_t], C.c_int),
 }

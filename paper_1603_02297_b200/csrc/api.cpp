@@ -17,6 +17,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "cache.hpp"
 #include "launch.hpp"
 #include "plan.hpp"
 #include "problem.hpp"
@@ -77,6 +78,7 @@ struct ttb_plan_s {
   int device = 0, sms = 148;
   std::string key;    // canonical_key + device
   bool cached = true;
+  float tuned_ms = 0.0f;  // best time of the last autotune
   // end-to-end staging (ttb_plan_execute_host)
   void* dA = nullptr;
   void* dB = nullptr;
@@ -608,6 +610,7 @@ int ttb_plan_autotune(ttb_plan plan, const void* A, void* B, int warmups, int re
     if (scratch) cudaFree(scratch);
     if (rc) return cuda_fail(cudaGetLastError(), "autotune");
     plan->prep = winner;
+    plan->tuned_ms = best;
     if (plan->cached) {
       std::lock_guard<std::mutex> lk(g_mu);
       g_choice[plan->key] = winner.spec.text();
@@ -617,6 +620,97 @@ int ttb_plan_autotune(ttb_plan plan, const void* A, void* B, int warmups, int re
     // beta == 0 every candidate overwrote it; with beta != 0 it is untouched)
     const int r2 = execute(plan, plan->prep, A, B, s, plan->orig.alpha, plan->orig.beta);
     if (r2) return r2;
+    return ok();
+  });
+}
+
+int ttb_cache_store(const char* file, const char* problem_key, const char* hardware_key,
+                    const char* plan_text, double bandwidth_gibs) {
+  return guarded([&] {
+    if (!file || !*file) return fail(TTB_EINVAL, "cache: no file");
+    cache_store(file, CacheEntry{problem_key ? problem_key : "", hardware_key ? hardware_key : "",
+                                 plan_text ? plan_text : "", bandwidth_gibs, iso8601_utc_now()});
+    return ok();
+  });
+}
+
+int ttb_cache_lookup(const char* file, const char* problem_key, const char* hardware_key,
+                     char* plan_buf, size_t plan_len, double* bandwidth_gibs, char* ts_buf,
+                     size_t ts_len, int* found) {
+  return guarded([&] {
+    if (!file || !problem_key || !hardware_key || !found)
+      return fail(TTB_EINVAL, "cache: null argument");
+    CacheEntry e;
+    *found = cache_lookup(file, problem_key, hardware_key, &e) ? 1 : 0;
+    if (!*found) return ok();
+    if (plan_buf) {
+      if (plan_len <= e.plan.size()) return fail(TTB_EINVAL, "cache: plan buffer too small");
+      std::memcpy(plan_buf, e.plan.c_str(), e.plan.size() + 1);
+    }
+    if (ts_buf) {
+      if (ts_len <= e.timestamp.size()) return fail(TTB_EINVAL, "cache: timestamp buffer too small");
+      std::memcpy(ts_buf, e.timestamp.c_str(), e.timestamp.size() + 1);
+    }
+    if (bandwidth_gibs) *bandwidth_gibs = e.bandwidth_gibs;
+    return ok();
+  });
+}
+
+int ttb_hardware_key(char* buf, size_t len) {
+  return guarded([&] {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    cudaDeviceProp prop{};
+    if ((e = cudaGetDeviceProperties(&prop, dev)) != cudaSuccess)
+      return cuda_fail(e, "cudaGetDeviceProperties");
+    const std::string k = std::string(prop.name) + ":sm" + std::to_string(prop.major) +
+                          std::to_string(prop.minor) + ":" + std::to_string(prop.multiProcessorCount) +
+                          "sms:ttb" + TTB_VERSION;
+    if (!buf || len <= k.size()) return fail(TTB_EINVAL, "hardware key: buffer too small");
+    std::memcpy(buf, k.c_str(), k.size() + 1);
+    return ok();
+  });
+}
+
+int ttb_plan_tune_cached(ttb_plan plan, const char* cache_file, const void* A, void* B,
+                         int warmups, int reps, ttb_stream stream, int* hit) {
+  if (!plan) return fail(TTB_EINVAL, "plan: null handle");
+  return guarded([&] {
+    if (!cache_file || !*cache_file) return fail(TTB_EINVAL, "cache: no file");
+    char hk[512];
+    int rc = ttb_hardware_key(hk, sizeof hk);
+    if (rc) return rc;
+    const std::string pkey = cache_key(plan->orig);  // canonical_key of the original problem
+    CacheEntry e;
+    if (hit) *hit = 0;
+    if (cache_lookup(cache_file, pkey, hk, &e)) {
+      Spec sp;
+      Prepared pr;
+      if (Spec::parse(e.plan, &sp) && prepare(plan->geo, sp, plan->sms, &pr, nullptr)) {
+        plan->prep = pr;
+        if (hit) *hit = 1;
+        return execute(plan, plan->prep, A, B, reinterpret_cast<cudaStream_t>(stream),
+                       plan->orig.alpha, plan->orig.beta);
+      }
+    }
+    rc = ttb_plan_autotune(plan, A, B, warmups, reps, stream);
+    if (rc) return rc;
+    const Problem& p = plan->orig;
+    const double bytes = static_cast<double>(p.elements()) *
+                         (kind_bytes(p.kind_a) + kind_bytes(p.kind_b) * (p.beta != 0.0 ? 2 : 1));
+    const double gibs = bytes / 1073741824.0 / (std::max(plan->tuned_ms, 1e-6f) * 1e-3);
+    cache_store(cache_file, CacheEntry{pkey, hk, plan->prep.spec.text(), gibs, iso8601_utc_now()});
+    return ok();
+  });
+}
+
+int ttb_benchmark_manifest(int64_t volume_bytes, int kind, uint64_t seed, char* buf, size_t len) {
+  return guarded([&] {
+    std::string t;
+    for (const std::string& l : benchmark_manifest(volume_bytes, kind, seed)) t += l + "\n";
+    if (!buf || len <= t.size()) return fail(TTB_EINVAL, "benchmark: buffer too small");
+    std::memcpy(buf, t.c_str(), t.size() + 1);
     return ok();
   });
 }

@@ -33,11 +33,16 @@ METRICS = {
     "issue_active_pct": ("sm__inst_issued.avg.pct_of_peak_sustained_active", 1),
     "sm_throughput_pct": ("sm__throughput.avg.pct_of_peak_sustained_elapsed", 1),
     "grid": ("launch__grid_size", 1),
+    "inst_executed": ("smsp__inst_executed.sum", 1),
+    "smem_wavefronts": ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 1),
+    "l2_read_sectors": ("lts__t_sectors_op_read.sum", 1),
+    "l2_write_sectors": ("lts__t_sectors_op_write.sum", 1),
     "block": ("launch__block_size", 1),
 }
 
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1,
-         "usecond": 1e3, "msecond": 1e6, "second": 1e9}
+         "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9,
+         "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
 
 def raw(rep):
@@ -71,6 +76,17 @@ def main():
             elif u in UNITS and "bytes" in key:
                 v = v * UNITS[u]
             d[key] = v
+        stalls = []
+        for i, name in enumerate(hdr):
+            if name.startswith("smsp__average_warps_issue_stalled_") and \
+                    name.endswith("_per_issue_active.ratio"):
+                try:
+                    stalls.append((float(row[i].replace(",", "")),
+                                   name[len("smsp__average_warps_issue_stalled_"):-len(
+                                       "_per_issue_active.ratio")]))
+                except ValueError:
+                    pass
+        d["stalls"] = {k: round(v, 2) for v, k in sorted(stalls, reverse=True)[:6]}
         if "ld_requests" in d and d["ld_requests"]:
             d["ld_sectors_per_req"] = d["ld_sectors"] / d["ld_requests"]
         if "st_requests" in d and d["st_requests"]:

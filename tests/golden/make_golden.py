@@ -8,6 +8,8 @@ Writes:
                                          reference_transpose outputs (bytes)
   merge_validate.json                 -- reference merge_indices results and
                                          validate messages
+  benchmark_manifest.json             -- the reference's 57-case suite manifests
+                                         (build_benchmark, benchmark.cpp:166-220)
   config_checksums.json               -- u64 checksums (oracle/ttb_oracle.c
                                          orc_checksum) of the reference's output
                                          for every BASELINE config at full size
@@ -153,12 +155,27 @@ def config_checksums(co, ref, threads):
         json.dump(res, f, indent=1)
 
 
+# the paper's suite at its default volume (200 MiB) and two
+# more (kind, seed) points, as the reference's build_benchmark writes them
+MANIFESTS = [(200 << 20, "s", 42), (200 << 20, "d", 42), (64 << 20, "c", 7)]
+
+
+def benchmark_manifests(ref):
+    out = {f"{v >> 20}MiB_{k}_{s}": ref.benchmark_manifest(v, k, s) for v, k, s in MANIFESTS}
+    with open(os.path.join(HERE, "benchmark_manifest.json"), "w") as f:
+        json.dump(out, f, indent=0)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-configs", action="store_true")
+    ap.add_argument("--only", choices=["manifest"], default=None)
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
     args = ap.parse_args()
     co, ref = COracle(), RefOracle()
+    benchmark_manifests(ref)
+    if args.only == "manifest":
+        return
     small_cases(co, ref)
     merge_validate(ref)
     if not args.skip_configs:

@@ -346,3 +346,34 @@ def test_kernels_actually_launch():
     ttb.reference_transpose(p, a, b)
     torch.cuda.synchronize()
     assert ttb.launch_count() == before + 1
+
+
+def test_tune_cached_miss_then_hit(tmp_path, coracle):
+    """pipeline.cpp:102-185: first call autotunes and appends the winner under
+    (canonical key, hardware key); the second call is a hit that selects it;
+    a stale entry (plan that no longer applies) is re-tuned.  Output exact."""
+    rng = np.random.default_rng(77)
+    perm, sizes = [3, 1, 2], [40, 33, 20]
+    A, B = _inputs(coracle, rng, "s", "s", perm, sizes, None, None, 0.5)
+    want = B.copy()
+    coracle.transpose("s", "s", perm, sizes, None, None, 1.0, A, 0.5, want)
+    p = ttb.make_problem(perm, sizes, "s", "s", 1.0, 0.5)
+    f = tmp_path / "solutions.tsv"
+    hw = ttb.hardware_key()
+    assert "sm100" in hw and "sms:ttb" in hw
+    for expect_hit in (False, True):
+        dA, dB = _dev(A), _dev(B)
+        plan = ttb.GpuPlan(p, cache=False)
+        assert plan.tune_cached(dA, dB, f) is expect_hit
+        torch.cuda.synchronize()
+        assert dB.cpu().numpy().tobytes() == want.tobytes()
+        e = ttb.SolutionCache(f).lookup(ttb.canonical_key(p), hw)
+        assert e is not None and e.plan.startswith("kern=") and e.bandwidth_gibs > 0
+        assert plan.describe().startswith(e.plan)
+    assert len(f.read_text().splitlines()) == 1
+    ttb.SolutionCache(f).store(ttb.SolutionEntry(ttb.canonical_key(p), hw, "kern=bogus", 1.0))
+    dA, dB = _dev(A), _dev(B)
+    assert ttb.GpuPlan(p, cache=False).tune_cached(dA, dB, f) is False
+    torch.cuda.synchronize()
+    assert dB.cpu().numpy().tobytes() == want.tobytes()
+    assert len(f.read_text().splitlines()) == 3

@@ -50,9 +50,12 @@ __host__ __device__ inline uint32_t dense_stage_bytes(uint32_t tx, uint32_t ty, 
   return tables + tile_a + tile_b;
 }
 
+#ifndef TTB_DENSE_MINB
+#define TTB_DENSE_MINB 1
+#endif
 template <class SA, class SB, int C, int MODE, int EPT, int NS>
 __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == sizeof(SB))
-                                           ? 1
+                                           ? TTB_DENSE_MINB
                                            : 4) dense_kernel(const SmemParams P) {
   static_assert(EPT > 0 && NS >= 2, "dense tile");
   using E = Vec<SA, C>;

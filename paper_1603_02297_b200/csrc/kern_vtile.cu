@@ -12,8 +12,9 @@ namespace ttb {
 
 namespace {
 template <class F>
-cudaError_t with_vtile(int ka, int kb, int mode, int va, int vb, F&& f) {
+cudaError_t with_vtile(int ka, int kb, int mode, int va, int vb, int sh, F&& f) {
   if (ka != kb || ka > 2 || (va == 1 && vb == 1)) return cudaErrorInvalidValue;
+  if (sh < 0 || sh > 3) return cudaErrorInvalidValue;
   return with_types(ka, kb, [&](auto t) -> cudaError_t {
     using T = decltype(t);
     using SA = typename T::SA;
@@ -28,13 +29,22 @@ cudaError_t with_vtile(int ka, int kb, int mode, int va, int vb, F&& f) {
     };
     return modes([&](auto m) {
       constexpr int M = decltype(m)::value;
+      if (sh != 0) {  // shifted sides: full 16-byte vectors on both sides
+        constexpr int V = 16 / EB;
+        if (va != V || vb != V) return cudaErrorInvalidValue;
+        switch (sh) {
+          case 1: return f(&vtile_kernel<SA, SB, T::C, M, V, V, 1>);
+          case 2: return f(&vtile_kernel<SA, SB, T::C, M, V, V, 2>);
+          default: return f(&vtile_kernel<SA, SB, T::C, M, V, V, 3>);
+        }
+      }
       return with_width<EB>(va, [&](auto a) {
         return with_width<EB>(vb, [&](auto b) {
           constexpr int VA = decltype(a)::value, VB = decltype(b)::value;
           if constexpr (VA == 1 && VB == 1)
             return cudaErrorInvalidValue;
           else
-            return f(&vtile_kernel<SA, SB, T::C, M, VA, VB>);
+            return f(&vtile_kernel<SA, SB, T::C, M, VA, VB, 0>);
         });
       });
     });
@@ -45,7 +55,7 @@ cudaError_t with_vtile(int ka, int kb, int mode, int va, int vb, F&& f) {
 
 cudaError_t launch_vtile(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                          cudaStream_t s) {
-  return with_vtile(ka, kb, mode, p.va, p.vb, [&](auto fn) {
+  return with_vtile(ka, kb, mode, p.va, p.vb, p.sh, [&](auto fn) {
     if (l.smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
       if (e != cudaSuccess) return e;
@@ -56,9 +66,9 @@ cudaError_t launch_vtile(int ka, int kb, int mode, const SmemParams& p, const La
   });
 }
 
-int occupancy_vtile(int ka, int kb, int mode, int va, int vb, int block, int smem) {
+int occupancy_vtile(int ka, int kb, int mode, int va, int vb, int sh, int block, int smem) {
   int n = 0;
-  with_vtile(ka, kb, mode, va, vb, [&](auto fn) {
+  with_vtile(ka, kb, mode, va, vb, sh, [&](auto fn) {
     if (smem_carveout() >= 0)
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, smem_carveout());
     if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -24,7 +24,7 @@ int occupancy_smem(int ka, int kb, int mode, int dense, int ept, int block, int 
 // vtile_kernel (SmemParams::dense == 4), kern_vtile.cu
 cudaError_t launch_vtile(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                          cudaStream_t s);
-int occupancy_vtile(int ka, int kb, int mode, int va, int vb, int block, int smem);
+int occupancy_vtile(int ka, int kb, int mode, int va, int vb, int sh, int block, int smem);
 int smem_carveout();
 
 // data utilities (util.cu)

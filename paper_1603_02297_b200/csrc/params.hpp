@@ -115,6 +115,7 @@ struct SmemParams {
   uint32_t ltx, lty;
   int ept;                // dense with tx,ty <= 256 and tx*ty = 256*ept: fixed walks
   int va, vb;             // dense == 4 (vtile_kernel): vector widths along x in A / y in B
+  int sh;                 // dense == 4: bit 0 A rows shifted, bit 1 B columns shifted (vtile.cuh)
 };
 
 // Launch shape chosen by the planner.

@@ -184,6 +184,24 @@ bool vtile_widths(const Geo& g, const std::vector<int>& xs, const std::vector<in
   return *va * *vb > 1;
 }
 
+// shifted vtile (vec=2): full 16-byte vectors on both sides, a side whose
+// strides do not keep every tile row / column 16-byte aligned is shifted per
+// row / column (vtile.cuh SH bits); tile sides must be multiples of the vector
+bool vtile_shift(const Geo& g, const std::vector<int>& xs, const std::vector<int>& ys, int64_t tx,
+                 int64_t ty, int* v, int* sh) {
+  if (g.ka != g.kb || g.ka > 2 || !x_dense_in_a(g, xs) || !y_dense_in_b(g, ys)) return false;
+  const int V = 16 / g.eA;
+  if (tx % V || ty % V || tx / V + 1 > 256 || ty / V + 1 > 256) return false;
+  auto aligned = [&](const std::vector<int>& grp, const int64_t* st) {
+    for (int a = 0; a < g.r; ++a)
+      if (std::find(grp.begin(), grp.end(), a) == grp.end() && st[a] % V) return false;
+    return true;
+  };
+  *v = V;
+  *sh = (aligned(xs, g.sa) ? 0 : 1) | (aligned(ys, g.sb) ? 0 : 2);
+  return *sh != 0;
+}
+
 // row pitch of vtile_kernel's A tile: a multiple of VA (16-byte chunk
 // destinations) with the fewest shared-memory wavefronts for the store walk
 // (lane t reads rows yl..yl+VB-1 of column c0, yl = (t % (ty/VB))*VB, c0 = t / (ty/VB))
@@ -330,6 +348,8 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
       d.cost += 0.02;
       out->push_back(d);
     }
+    // (shifted vector tiles, vec=2, are selectable by plan text but not offered:
+    // measured slower than the element-wise kernels on every misaligned c5 row)
     // power-of-two tiles of 4-16 warps' worth may run on dense_kernel: offer
     // its three-stage cp.async ring as well (prepare() decides applicability)
     const Spec& c = cand[i];
@@ -685,8 +705,10 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
       return fail("smem: index space exceeds 2^31");
     m.S = shared ? static_cast<uint32_t>(g.n[0]) : 1;
     if (s.tx < 1 || s.ty < 1 || s.tx > 4096 || s.ty > 4096) return fail("smem: bad tile");
-    m.tx = static_cast<uint32_t>(std::min<int64_t>(s.tx, m.X.total));
-    m.ty = static_cast<uint32_t>(std::min<int64_t>(s.ty, m.Y.total));
+    // a shifted vector tile keeps whole vectors per side (partial tiles are masked)
+    const int64_t vq = s.vec == 2 ? 16 / g.eA : 1;
+    m.tx = static_cast<uint32_t>(std::min<int64_t>(s.tx, (m.X.total + vq - 1) / vq * vq));
+    m.ty = static_cast<uint32_t>(std::min<int64_t>(s.ty, (m.Y.total + vq - 1) / vq * vq));
     // tile_kernel: 32-bit offset tables and one tile row / column per thread
     // position; otherwise the general 64-bit smem_kernel
     const bool small = g.foot_a < (int64_t{1} << 31) && g.foot_b < (int64_t{1} << 31);
@@ -710,8 +732,18 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     m.va = m.vb = 1;
     // vector tile: every A tile row starts on a VA boundary, every B tile
     // column on a VB boundary (vtile.cuh); equal kinds s/d/c, two stages
-    int va = 1, vb = 1;
-    if (s.vec && s.st == 2 && small && m.S == 1 && vtile_widths(g, xs, ys, m.tx, m.ty, &va, &vb)) {
+    int va = 1, vb = 1, sh = 0;
+    m.sh = 0;
+    if (s.vec == 2) {
+      if (!(s.st == 2 && small && m.S == 1 && vtile_shift(g, xs, ys, m.tx, m.ty, &va, &sh)))
+        return fail("smem: shifted vector tile not applicable");
+      m.dense = 4;
+      m.ept = 0;
+      m.va = m.vb = va;
+      m.sh = sh;
+      m.rl = vtile_row_length(m.tx + ((sh & 1) ? va : 0), m.ty + ((sh & 2) ? va : 0), va, va, g.eA);
+    } else if (s.vec && s.st == 2 && small && m.S == 1 &&
+               vtile_widths(g, xs, ys, m.tx, m.ty, &va, &vb)) {
       m.dense = 4;
       m.ept = 0;
       m.va = va;
@@ -736,17 +768,21 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
         m.dense ? (m.dense == 3 ? 3 : 2) *  // pipeline stages (dense_stage_bytes in dense.cuh)
                       (r16(static_cast<int64_t>(m.tx + m.ty) * (m.dense >= 2 ? 4 : 8)) +
                        r16(static_cast<int64_t>(m.ty) * m.rl * g.eA) +
-                       (p.mode == 2 ? r16(static_cast<int64_t>(m.S) * m.tx * m.ty * g.eB) : 0))
+                       (p.mode == 2 ? r16(static_cast<int64_t>(m.S) * m.tx *
+                                          (m.ty + ((m.sh & 2) ? m.vb : 0)) * g.eB)
+                                    : 0))
                 : static_cast<int64_t>(m.tx + m.ty) * 2 * 8 + static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);
     const int occ = std::min(
-        occ_cap, std::max(1, m.dense == 4 ? occupancy_vtile(g.ka, g.kb, p.mode, m.va, m.vb, 256, p.l.smem)
+        occ_cap, std::max(1, m.dense == 4 ? occupancy_vtile(g.ka, g.kb, p.mode, m.va, m.vb, m.sh, 256, p.l.smem)
                                           : occupancy_smem(g.ka, g.kb, p.mode, m.dense, m.ept, 256,
                                                            p.l.smem)));
     p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(m.items, int64_t{occ} * sms)));
-    p.a_align = std::min(16, g.eA * m.va);  // whole elements (Vec<SA, C>) / vectors move as a unit
-    p.b_align = std::min(16, g.eB * m.vb);
+    // whole elements (Vec<SA, C>) / vectors move as a unit; shifted tiles
+    // compute the shift from element offsets, so the bases must be 16-B aligned
+    p.a_align = m.sh ? 16 : std::min(16, g.eA * m.va);
+    p.b_align = m.sh ? 16 : std::min(16, g.eB * m.vb);
   }
   p.l.block = 256;
   *out = p;

@@ -175,6 +175,12 @@ def test_vector_tile_shapes(coracle, kind):
         ([2, 3, 1], [36, 5, 10], None, None),
         ([5, 2, 4, 1, 3], [10, 8, 3, 36, 2], None, None),
         ([4, 3, 1, 2], [12, 9, 4, 14], [12, 10, 4, 14], [4, 15, 9, 12]),
+        # odd extents: rows / columns at arbitrary offsets (shifted tiles, vec=2)
+        ([2, 1], [37, 45], None, None),
+        ([3, 1, 2], [19, 21, 7], None, None),
+        ([2, 3, 1], [35, 3, 33], None, None),
+        ([2, 1], [41, 29], [43, 29], [30, 41]),
+        ([3, 2, 1], [7, 9, 11], None, None),
     ]
     seen = 0
     for perm, sizes, lda, ldb in cases:
@@ -190,8 +196,10 @@ def test_vector_tile_shapes(coracle, kind):
                 got = run_gpu(kind, kind, perm, sizes, lda, ldb, alpha, A, beta, B, plan_text=text)
                 assert got.tobytes() == want.tobytes(), (perm, sizes, alpha, beta, text)
             # explicit vector tiles (tile sides that are multiples of the vector width)
-            for tx, ty in [(16, 12), (20, 8), (32, 32), (12, 36)]:
-                text = f"kern=smem;kx=1;ky=1;tx={tx};ty={ty};order=0;occ=0;st=2;bp={int(beta != 0)};vec=1"
+            for tx, ty, vec in [(16, 12, 1), (20, 8, 1), (32, 32, 1), (12, 36, 1), (16, 12, 2),
+                                (32, 8, 2), (8, 32, 2), (64, 64, 2)]:
+                bp = int(beta != 0) if (tx + ty) % 3 else 0
+                text = f"kern=smem;kx=1;ky=1;tx={tx};ty={ty};order=0;occ=0;st=2;bp={bp};vec={vec}"
                 plan = ttb.GpuPlan(p, cache=False)
                 try:
                     plan.select(text)

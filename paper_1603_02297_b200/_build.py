@@ -80,7 +80,26 @@ def build(verbose: bool = False) -> str:
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
         os.replace(LIB + ".tmp", LIB)
+    _build_cli()
     return LIB
+
+
+CLI_SRC = os.path.join(PKG, "tools", "ttb_cli.cpp")
+CLI = os.path.join(LIBDIR, "ttb")
+
+
+def _build_cli() -> None:
+    """tools/ttb_cli.cpp -> _lib/ttb, a C-ABI client of libttb.so (rpath $ORIGIN)."""
+    if os.path.exists(CLI) and os.path.getmtime(CLI) >= max(
+            os.path.getmtime(CLI_SRC), os.path.getmtime(LIB),
+            os.path.getmtime(os.path.join(ROOT, "include", "ttb.h"))):
+        return
+    cmd = [_nvcc(), "-std=c++17", "-O2", "-ccbin", _host_cxx(), "-I", os.path.join(ROOT, "include"),
+           CLI_SRC, "-o", CLI + ".tmp", "-L", LIBDIR, "-lttb", "-Xlinker", "-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"cli build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    os.replace(CLI + ".tmp", CLI)
 
 
 def build_variant(name: str, defines: list, only=None) -> str:

@@ -590,7 +590,21 @@ std::vector<Spec> candidates(const Geo& g) {
       fallback.vec = 0;
       have_fb = true;
     }
-  if (out.size() > 32) out.resize(32);
+  // cap the list but keep every family represented: the best few copy and
+  // register-transpose candidates survive even when staged tiles rank higher
+  if (out.size() > 32) {
+    std::vector<Spec> kept(out.begin(), out.begin() + 32);
+    for (Variant v : {kCopy, kRt}) {
+      int have = 0;
+      for (const Spec& k : kept) have += k.v == v;
+      for (size_t i = 32; i < out.size() && have < 4; ++i)
+        if (out[i].v == v) {
+          kept.push_back(out[i]);
+          ++have;
+        }
+    }
+    out.swap(kept);
+  }
   if (have_fb) out.push_back(fallback);
   return out;
 }

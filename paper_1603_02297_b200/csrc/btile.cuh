@@ -1,0 +1,265 @@
+// btile.cuh -- the staged tile fed by the Blackwell bulk-copy (TMA) engine.
+//
+// Same tile as dense_kernel / vtile_kernel (S == 1, X group contiguous in A,
+// Y group contiguous in B -- ttune's run_case2, executor.cpp:213-281), but the
+// global -> shared side is one cp.async.bulk per tile row instead of one
+// LDGSTS per element or 16-byte chunk, and the kernel is warp specialised:
+//
+//   warps NC..NC+PW-1   (producers) for every tile of this CTA: wait until the ring stage
+//                       is free, decode the tile's row / column offsets (one
+//                       lane per row / column), issue a bulk copy of each A
+//                       tile row -- and with beta != 0 of each B tile column --
+//                       into the stage, write the offset tables, arrive on the
+//                       stage's `full` mbarrier with the byte count.
+//   warps 0..NC-1       wait on `full`, write the tile to B with lanes along
+//                       B's stride-1 index (coalesced stores, alpha/beta
+//                       epilogue fused), release the stage on `empty`.
+//
+// Bulk copies need 16-byte aligned addresses and sizes: a row that starts or
+// ends inside a 16-byte block is fetched as the aligned superset of blocks that
+// covers it (at most 12 bytes either side, never outside the blocks that hold
+// the row's own first and last element, so never outside the allocation) and
+// its elements land in shared memory shifted by d(y) = (row start mod 16) /
+// element bytes; the consumer reads element x of row y at y*pitch + d(y) + x.
+// Bytes of the superset outside the logical row are never used.
+//
+// The ring has NS stages (NS - 1 tiles of loads in flight while a tile is
+// written out), so the bytes in flight per SM are set by shared memory, not by
+// registers or by how many threads issue loads -- the element-wise kernels
+// (dense_kernel, tile_kernel) stall on exactly that with misaligned f32 rows.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace ttb {
+
+constexpr int kBtileMaxStages = 8;
+constexpr int kBtileConsumerWarps = 4;
+// bulk copies are issued per warp through the uniform datapath (one lane's
+// copy at a time), so the issue rate scales with producer warps, not lanes
+constexpr int kBtileProducerWarps = 2;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.release.cta.shared::cta.b64 st, [%0]; }" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+// arrive and add `bytes` to the phase's expected transaction count (the
+// copies it covers may already have completed: tx-count may go negative)
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{ .reg .b64 st; mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1; }" ::"r"(
+          smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+
+// spin on mbarrier.test_wait (non-blocking): try_wait may suspend the thread
+// for a system-dependent time after the phase completes
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef TTB_BTILE_TRYWAIT
+  asm volatile(
+      "{\n"
+      " .reg .pred done;\n"
+      "W: mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n"
+      " @!done bra W;\n"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#else
+  asm volatile(
+      "{\n"
+      " .reg .pred done;\n"
+      "W: mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n"
+      " @!done bra W;\n"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#endif
+}
+
+// global -> shared bulk copy (TMA engine, no tensor map), completion counted
+// in bytes on `bar`; dst, src and bytes are multiples of 16
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// (stage layout: btile_stage_bytes, params.hpp)
+
+// P.ns stages, P.pa / P.pb row / column pitches (bytes), P.ly lanes along y
+// (power of two <= 32; 32 / ly columns per warp step), JY = tile rows per lane
+// (ty <= JY * ly).  MODE 0/1/2 as Update.
+// EXP (kernel-design probes only, scripts/btile_probe.cu): bit 0 skips the B
+// stores, bit 1 skips the bulk copies (the ring still cycles), bit 2 skips the
+// consumers' work (they only wait and release)
+template <class SA, class SB, int C, int MODE, int JY, int PW = kBtileProducerWarps,
+          int NC = kBtileConsumerWarps, int EXP = 0>
+__global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams P) {
+  using E = Vec<SA, C>;
+  using EBv = Vec<SB, C>;
+  constexpr uint32_t EA = sizeof(E), EB = sizeof(EBv);
+  constexpr bool UPD = MODE == 2;
+  // columns per consumer step: ~4 words of loads in flight per tile row
+  constexpr int UX = EB <= 4 ? 4 : EB <= 8 ? 2 : 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint64_t full[kBtileMaxStages], empty[kBtileMaxStages];
+
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t NS = P.ns;
+  const uint32_t tables = btile_tables_bytes(P.tx, P.ty, UPD);
+  const uint32_t stage_bytes = btile_stage_bytes(P.tx, P.ty, P.pa, P.pb, UPD);
+  auto stage = [&](uint32_t s) { return smem_raw + s * stage_bytes; };
+
+  if (tid == 0) {
+    for (uint32_t s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 32 * PW);  // every producer lane arrives (with its bytes)
+      mbar_init(&empty[s], NC);  // one arrival per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const uint32_t g = gridDim.x;
+  if (warp >= NC) {
+    // ------------------------------------------------------------ producer --
+    const unsigned char* A = static_cast<const unsigned char*>(P.A);
+    const unsigned char* Bc = static_cast<const unsigned char*>(P.B);
+    uint32_t s = 0, ph = 0;
+    for (uint32_t it = blockIdx.x; it < P.items; it += g) {
+      mbar_wait(&empty[s], ph ^ 1);  // a fresh barrier passes parity 1 at once
+      const DenseTile t = dense_tile(P, it);
+      int64_t aO, bO;
+      decode(P.O, t.o, aO, bO);
+      unsigned char* st = stage(s);
+      uint32_t* rbase = reinterpret_cast<uint32_t*>(st);
+      uint32_t* boff = rbase + P.ty;
+      uint32_t* cbase = boff + P.tx;
+      unsigned char* ta = st + tables;
+      unsigned char* tb = ta + P.ty * P.pa;
+      uint32_t bytes = 0;
+      const uint32_t pl = (warp - NC) * 32 + lane;  // producer lane
+      for (uint32_t y = pl; y < t.ny; y += 32 * PW) {
+        int64_t a, b;
+        decode(P.Y, t.y0 + y, a, b);
+        const uint64_t start = reinterpret_cast<uint64_t>(A + (a + aO + t.x0) * EA);
+        const uint64_t lo = start & ~uint64_t{15};
+        const uint64_t hi = (start + t.nx * EA + 15) & ~uint64_t{15};
+        const uint32_t n = static_cast<uint32_t>(hi - lo);
+        if constexpr (!(EXP & 2)) {
+          bulk_g2s(ta + y * P.pa, reinterpret_cast<const void*>(lo), n, &full[s]);
+          bytes += n;
+        }
+        rbase[y] = (y * P.pa + static_cast<uint32_t>(start - lo)) / EA;
+      }
+      for (uint32_t x = pl; x < t.nx; x += 32 * PW) {
+        int64_t a, b;
+        decode(P.X, t.x0 + x, a, b);
+        const int64_t bo = b + bO + t.y0;
+        boff[x] = static_cast<uint32_t>(bo);
+        if constexpr (UPD) {
+          const uint64_t start = reinterpret_cast<uint64_t>(Bc + bo * EB);
+          const uint64_t lo = start & ~uint64_t{15};
+          const uint64_t hi = (start + t.ny * EB + 15) & ~uint64_t{15};
+          const uint32_t n = static_cast<uint32_t>(hi - lo);
+          bulk_g2s(tb + x * P.pb, reinterpret_cast<const void*>(lo), n, &full[s]);
+          bytes += n;
+          cbase[x] = (x * P.pb + static_cast<uint32_t>(start - lo)) / EB;
+        }
+      }
+      mbar_arrive_expect_tx(&full[s], bytes);
+      if (++s == NS) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers --
+  const Update<SA, SB, MODE> up(P.sc);
+  EBv* __restrict__ B = static_cast<EBv*>(P.B);
+  const uint32_t ly = P.ly, lxn = 32u / ly;
+  const uint32_t yi = lane & (ly - 1), xi = lane / ly;
+  const uint32_t xstep = NC * lxn;
+  uint32_t s = 0, ph = 0;
+  for (uint32_t it = blockIdx.x; it < P.items; it += g) {
+    const DenseTile t = dense_tile(P, it);
+    mbar_wait(&full[s], ph);
+    const unsigned char* st = stage(s);
+    const uint32_t* rbase = reinterpret_cast<const uint32_t*>(st);
+    const uint32_t* boff = rbase + P.ty;
+    const uint32_t* cbase = boff + P.tx;
+    const E* ta = reinterpret_cast<const E*>(st + tables);
+    const EBv* tb = reinterpret_cast<const EBv*>(st + tables + P.ty * P.pa);
+    // this lane's JY tile rows (y = yi + j*ly) are fixed for the tile; UX
+    // columns per step, all loads of a step issued before its stores
+    uint32_t rb[JY];
+    bool yv[JY];
+#pragma unroll
+    for (int j = 0; j < JY; ++j) {
+      const uint32_t y = yi + j * ly;
+      yv[j] = y < t.ny;
+      rb[j] = yv[j] ? rbase[y] : 0u;
+    }
+    for (uint32_t x0 = warp * lxn + xi; x0 < ((EXP & 4) ? 0u : t.nx); x0 += UX * xstep) {
+      EBv* q[UX];
+      uint32_t xs[UX], cb[UX];
+      bool xv[UX];
+#pragma unroll
+      for (int u = 0; u < UX; ++u) {
+        const uint32_t x = x0 + u * xstep;
+        xv[u] = x < t.nx;
+        xs[u] = xv[u] ? x : x0;
+        q[u] = B + boff[xs[u]] + yi;
+        if constexpr (UPD) cb[u] = cbase[xs[u]];
+      }
+      EBv w[UX][JY];
+#pragma unroll
+      for (int u = 0; u < UX; ++u)
+#pragma unroll
+        for (int j = 0; j < JY; ++j) {
+          const E a = ta[rb[j] + xs[u]];
+          if constexpr (UPD) {
+            const EBv b = tb[cb[u] + (yv[j] ? yi + j * ly : 0u)];  // stay inside the column
+#pragma unroll
+            for (int c = 0; c < C; ++c) w[u][j].v[c] = up(a.v[c], b.v[c]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < C; ++c) w[u][j].v[c] = up(a.v[c], SB(0));
+          }
+        }
+#pragma unroll
+      for (int u = 0; u < UX; ++u)
+#pragma unroll
+        for (int j = 0; j < JY; ++j) {
+          if constexpr (EXP & 1) {
+            if (w[u][j].v[0] == SB(1234.5)) vstore_pred(q[u][j * ly].v, w[u][j], xv[u] && yv[j]);
+          } else {
+            vstore_pred(q[u][j * ly].v, w[u][j], xv[u] && yv[j]);
+          }
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == NS) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
+}
+
+}  // namespace ttb

@@ -23,17 +23,7 @@ struct DenseTile {
 __device__ __forceinline__ DenseTile dense_tile(const SmemParams& P, uint32_t it) {
   DenseTile t;
   uint32_t xc, yc;
-  if (P.order == 0) {
-    const uint32_t q = udiv(it, P.dnx);
-    xc = it - q * P.nxc;
-    t.o = udiv(q, P.dny);
-    yc = q - t.o * P.nyc;
-  } else {
-    const uint32_t q = udiv(it, P.dny);
-    yc = it - q * P.nyc;
-    t.o = udiv(q, P.dnx);
-    xc = q - t.o * P.nxc;
-  }
+  smem_tile_coords(P, it, xc, yc, t.o);
   t.x0 = xc * P.tx;
   t.y0 = yc * P.ty;
   t.nx = min(P.tx, P.X.total - t.x0);

@@ -1,0 +1,63 @@
+// kern_btile.cu -- instantiation and launch of btile_kernel (btile.cuh): the
+// four same-kind pairs (mixed pairs run on the other staged tiles), update
+// modes 0/1/2 (beta != 0 always stages B through the bulk-copy ring), 1/2/4/8
+// tile rows per consumer lane.
+#include <type_traits>
+
+#include "btile.cuh"
+#include "dispatch.cuh"
+#include "kernels.cuh"
+#include "launch.hpp"
+
+namespace ttb {
+
+namespace {
+template <class F>
+cudaError_t with_btile(int ka, int kb, int mode, int jy, F&& f) {
+  if (mode == 3) mode = 2;
+  if (ka != kb) return cudaErrorInvalidValue;
+  return with_types(ka, kb, [&](auto t) -> cudaError_t {
+    using T = decltype(t);
+    if constexpr (!std::is_same<typename T::SA, typename T::SB>::value) {
+      return cudaErrorInvalidValue;
+    } else {
+      return with_mode(mode, [&](auto m) {
+        constexpr int M = decltype(m)::value;
+        using SA = typename T::SA;
+        switch (jy) {
+          case 1: return f(&btile_kernel<SA, SA, T::C, M, 1>);
+          case 2: return f(&btile_kernel<SA, SA, T::C, M, 2>);
+          case 4: return f(&btile_kernel<SA, SA, T::C, M, 4>);
+          case 8: return f(&btile_kernel<SA, SA, T::C, M, 8>);
+          default: return cudaErrorInvalidValue;
+        }
+      });
+    }
+  });
+}
+}  // namespace
+
+cudaError_t launch_btile(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
+                         cudaStream_t s) {
+  return with_btile(ka, kb, mode, btile_rows_per_lane(p.ty, p.ly), [&](auto fn) {
+    if (l.smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
+      if (e != cudaSuccess) return e;
+    }
+    fn<<<l.grid, l.block, l.smem, s>>>(p);
+    count_launch();
+    return cudaGetLastError();
+  });
+}
+
+int occupancy_btile(int ka, int kb, int mode, int jy, int block, int smem) {
+  int n = 0;
+  with_btile(ka, kb, mode, jy, [&](auto fn) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem);
+  });
+  return n;
+}
+
+}  // namespace ttb

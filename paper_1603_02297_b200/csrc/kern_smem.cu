@@ -66,6 +66,7 @@ int smem_carveout() {
 cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                         cudaStream_t s) {
   if (p.dense == 4) return launch_vtile(ka, kb, mode, p, l, s);
+  if (p.dense == 5) return launch_btile(ka, kb, mode, p, l, s);
   return with_smem(ka, kb, mode, p.dense, p.ept, [&](auto fn) {
     if (l.smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);

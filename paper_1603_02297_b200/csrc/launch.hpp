@@ -26,6 +26,10 @@ cudaError_t launch_vtile(int ka, int kb, int mode, const SmemParams& p, const La
                          cudaStream_t s);
 int occupancy_vtile(int ka, int kb, int mode, int va, int vb, int sh, int block, int smem);
 int smem_carveout();
+// btile_kernel (SmemParams::dense == 5, bulk-copy ring), kern_btile.cu
+cudaError_t launch_btile(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
+                         cudaStream_t s);
+int occupancy_btile(int ka, int kb, int mode, int jy, int block, int smem);
 
 // data utilities (util.cu)
 struct BoxParams {

@@ -111,12 +111,40 @@ struct SmemParams {
   uint32_t items;
   // dense fast path: S == 1, X contiguous in A, Y contiguous in B, tx/ty powers
   // of two -> the walks need shifts and masks only, no per-element division
-  int dense;              // 0 generic, 1 dense (any tile), 2/3 dense power-of-two tile, 4 vector tile
+  int dense;              // 0 generic, 1 dense (any tile), 2/3 dense power-of-two tile, 4 vector tile,
+                          // 5 bulk-copy tile
   uint32_t ltx, lty;
   int ept;                // dense with tx,ty <= 256 and tx*ty = 256*ept: fixed walks
   int va, vb;             // dense == 4 (vtile_kernel): vector widths along x in A / y in B
   int sh;                 // dense == 4: bit 0 A rows shifted, bit 1 B columns shifted (vtile.cuh)
+  // dense == 5 (btile_kernel, bulk-copy ring): stages, A row / B column pitch
+  // in shared memory (bytes, multiples of 16), consumer lanes along y
+  uint32_t ns, pa, pb, ly;
+  // order >= 2: tiles walked in groups of `order` tile rows (Y chunks), X
+  // chunks next, so the tiles in flight at once form a block whose A rows and
+  // B columns continue across tiles (longer DRAM runs on both sides)
+  uint32_t grp;
+  Div32 dplane, dgrp, dG;  // nxc*nyc, grp*nxc, grp
 };
+
+// btile_kernel shared-memory layout of one stage (all offsets 16-byte aligned):
+//   rbase[ty]  u32: element index of tile row y's first element in the A tile
+//   boff[tx]   u32: B element offset of tile column x's first element
+//   cbase[tx]  u32: (beta != 0) element index of column x in the B tile
+//   A tile     ty rows of pa bytes
+//   B tile     (beta != 0) tx columns of pb bytes
+TTB_HD uint32_t btile_tables_bytes(uint32_t tx, uint32_t ty, bool upd) {
+  return ((ty + tx * (upd ? 2u : 1u)) * 4u + 15u) & ~15u;
+}
+TTB_HD uint32_t btile_stage_bytes(uint32_t tx, uint32_t ty, uint32_t pa, uint32_t pb, bool upd) {
+  return btile_tables_bytes(tx, ty, upd) + ty * pa + (upd ? tx * pb : 0u);
+}
+
+// btile_kernel tile rows per consumer lane (template JY: 1, 2, 4 or 8)
+TTB_HD int btile_rows_per_lane(uint32_t ty, uint32_t ly) {
+  const uint32_t n = (ty + ly - 1) / ly;
+  return n <= 1 ? 1 : n <= 2 ? 2 : n <= 4 ? 4 : 8;
+}
 
 // Launch shape chosen by the planner.
 struct Launch {

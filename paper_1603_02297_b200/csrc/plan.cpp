@@ -252,6 +252,8 @@ bool y_dense_in_b(const Geo& g, const std::vector<int>& ys) {
 
 // staged-tile candidates over every admissible pair of X / Y groups
 void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
+  std::vector<Spec> bulk_specs;
+  std::vector<Spec>* bulk = &bulk_specs;
   const int start = shared ? 1 : 0;
   if (g.r <= start) return;
   const int64_t S = shared ? g.n[0] : 1;
@@ -281,6 +283,47 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
       std::vector<int64_t> txs, tys;
       sides(NX, &txs);
       sides(NY, &tys);
+      if (!shared && fast && g.ka == g.kb && x_dense_in_a(g, xs) && y_dense_in_b(g, ys)) {
+        // bulk-copy tiles (btile.cuh): sides 32..256 (or the whole group),
+        // 8-64 KB of tile, as many ring stages as fit one or two CTAs per SM
+        auto bsides = [](int64_t N) {
+          std::vector<int64_t> v;
+          for (int64_t t : {32, 64, 128, 256})
+            if (t < N) v.push_back(t);
+          if (N <= 256) v.push_back(N);
+          return v;
+        };
+        for (int64_t tx : bsides(NX)) {
+          for (int64_t ty : bsides(NY)) {
+            const int64_t bytes = tx * ty * std::max(g.eA, g.eB);
+            if (bytes > 64 * 1024 || (bytes < 8 * 1024 && !(tx >= NX && ty >= NY))) continue;
+            const double ex = static_cast<double>(NX) / (((NX + tx - 1) / tx) * tx);
+            const double ey = static_cast<double>(NY) / (((NY + ty - 1) / ty) * ty);
+            const int64_t run_a = tx * g.eA, run_b = ty * g.eB;
+            auto run_cost = [](int64_t r) { return r < 64 ? 4.0 : r < 128 ? 1.5 : r < 256 ? 0.5 : 0.0; };
+            const int64_t stage = (tx + ty * 2) * 4 + ty * (tx * g.eA + 32) +
+                                  (g.mode == 2 ? tx * (ty * g.eB + 16) : 0);
+            // a CTA keeps about one stage of bulk copies moving at a time, so
+            // throughput comes from 3-6 CTAs per SM with 2-3 stages each
+            for (int64_t ns : {int64_t{3}, int64_t{2}}) {
+              if (ns * stage > 110 * 1024) continue;
+              const int64_t budget = ns == 3 ? 200 * 1024 : 100 * 1024;
+              Spec b;
+              b.v = kSmem;
+              b.kx = kx;
+              b.ky = ky;
+              b.tx = static_cast<int>(tx);
+              b.ty = static_cast<int>(ty);
+              b.vec = 3;
+              b.st = static_cast<int>(ns);
+              b.cost = 1.0 + (1.0 - ex * ey) * 12.0 + run_cost(run_a) + run_cost(run_b) +
+                       std::fabs(std::log2(static_cast<double>(bytes) / 16384.0)) * 0.2 +
+                       0.05 * (kx + ky) + (budget < 200 * 1024 ? 0.02 : 0.0);
+              bulk->push_back(b);
+            }
+          }
+        }
+      }
       for (int64_t tx : txs) {
         for (int64_t ty : tys) {
           const int64_t bytes = S * tx * ty * g.eA;
@@ -325,6 +368,9 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
   }
   std::stable_sort(cand.begin(), cand.end(),
                    [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
+  std::stable_sort(bulk_specs.begin(), bulk_specs.end(),
+                   [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
+  for (size_t i = 0; i < bulk_specs.size() && i < 6; ++i) out->push_back(bulk_specs[i]);
   for (size_t i = 0; i < cand.size() && i < 8; ++i) {
     out->push_back(cand[i]);
     int va, vb;
@@ -559,10 +605,15 @@ std::vector<Spec> candidates(const Geo& g) {
   smem_candidates(g, shared, &out);
   std::stable_sort(out.begin(), out.end(),
                    [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
-  // the tile order alternative of the best two transposing candidates
+  // the tile order alternative of the best two transposing candidates of
+  // each family (bulk-copy tiles, other tiles / register transposes)
   std::vector<Spec> extra;
-  for (size_t i = 0; i < out.size() && extra.size() < 2; ++i)
+  int n_bulk = 0, n_other = 0;
+  for (size_t i = 0; i < out.size(); ++i)
     if (out[i].v != kCopy) {
+      int& n = (out[i].v == kSmem && out[i].vec == 3) ? n_bulk : n_other;
+      if (n >= 2) continue;
+      ++n;
       Spec s = out[i];
       s.order = 1;
       s.cost += 0.01;
@@ -585,7 +636,7 @@ std::vector<Spec> candidates(const Geo& g) {
   Spec fallback;
   bool have_fb = false;
   for (const Spec& s : out)
-    if (!have_fb && (s.v == kSmem || (s.v == kCopy && s.w1 == 1))) {
+    if (!have_fb && ((s.v == kSmem && s.vec != 3) || (s.v == kCopy && s.w1 == 1))) {
       fallback = s;
       fallback.vec = 0;
       have_fb = true;
@@ -748,7 +799,30 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     // column on a VB boundary (vtile.cuh); equal kinds s/d/c, two stages
     int va = 1, vb = 1, sh = 0;
     m.sh = 0;
-    if (s.vec == 2) {
+    m.ns = m.pa = m.pb = 0;
+    m.ly = 32;
+    if (s.vec == 3) {
+      // bulk-copy tile (btile.cuh): one cp.async.bulk per A row (and B column
+      // when beta != 0), any element alignment, warp-specialised ring
+      if (!(small && m.S == 1 && g.ka == g.kb && x_dense_in_a(g, xs) && y_dense_in_b(g, ys)))
+        return fail("smem: bulk tile needs equal kinds, contiguous X in A and Y in B");
+      if (m.tx > 256 || m.ty > 256) return fail("smem: bulk tile side above 256");
+      if (s.st < 2 || s.st > 8) return fail("smem: bulk tile stages outside 2..8");
+      m.dense = 5;
+      m.ept = 0;
+      m.ly = 1;
+      while (m.ly < 32 && m.ly < m.ty) m.ly *= 2;
+      // a row's 16-byte superset spans at most tx*e + 16 - e bytes; an odd
+      // number of 16-byte units keeps 8 consecutive rows on distinct banks
+      auto pitch = [](uint32_t n, int e) {
+        uint32_t b = (n * static_cast<uint32_t>(e) + 16u - static_cast<uint32_t>(std::min(e, 16)) + 15u) & ~15u;
+        return b;
+      };
+      m.pa = pitch(m.tx, g.eA);
+      if ((m.pa / 16) % 2 == 0) m.pa += 16;
+      m.pb = pitch(m.ty, g.eB);
+      m.ns = static_cast<uint32_t>(s.st);
+    } else if (s.vec == 2) {
       if (!(s.st == 2 && small && m.S == 1 && vtile_shift(g, xs, ys, m.tx, m.ty, &va, &sh)))
         return fail("smem: shifted vector tile not applicable");
       m.dense = 4;
@@ -774,11 +848,17 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     m.order = s.order;
     const uint64_t items = uint64_t{m.nxc} * m.nyc * m.O.total;
     if (items >= kIdxLimit) return fail("smem: too many tiles");
+    if (s.order < 0 || s.order > 64) return fail("smem: bad tile order");
+    m.grp = s.order >= 2 ? static_cast<uint32_t>(s.order) : 1u;
+    m.dplane = Div32::make(m.nxc * m.nyc);
+    m.dgrp = Div32::make(m.grp * m.nxc);
+    m.dG = Div32::make(m.grp);
     m.items = static_cast<uint32_t>(items);
     // beta != 0 without the B ring: kernel mode 3 (staged-tile kernels only)
     if (g.mode == 2 && s.bp == 0 && m.dense) p.mode = 3;
     const auto r16 = [](int64_t v) { return (v + 15) & ~int64_t{15}; };
     const int64_t smem =
+        m.dense == 5 ? static_cast<int64_t>(m.ns) * btile_stage_bytes(m.tx, m.ty, m.pa, m.pb, g.mode == 2) :
         m.dense ? (m.dense == 3 ? 3 : 2) *  // pipeline stages (dense_stage_bytes in dense.cuh)
                       (r16(static_cast<int64_t>(m.tx + m.ty) * (m.dense >= 2 ? 4 : 8)) +
                        r16(static_cast<int64_t>(m.ty) * m.rl * g.eA) +
@@ -788,8 +868,13 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
                 : static_cast<int64_t>(m.tx + m.ty) * 2 * 8 + static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);
+    if (m.dense == 5) {
+      p.mode = g.mode;  // beta != 0 always stages B through the ring
+      p.l.block = 32 * 6;  // kBtileConsumerWarps + kBtileProducerWarps (btile.cuh)
+    }
     const int occ = std::min(
-        occ_cap, std::max(1, m.dense == 4 ? occupancy_vtile(g.ka, g.kb, p.mode, m.va, m.vb, m.sh, 256, p.l.smem)
+        occ_cap, std::max(1, m.dense == 5 ? occupancy_btile(g.ka, g.kb, p.mode, btile_rows_per_lane(m.ty, m.ly), p.l.block, p.l.smem) :
+                             m.dense == 4 ? occupancy_vtile(g.ka, g.kb, p.mode, m.va, m.vb, m.sh, 256, p.l.smem)
                                           : occupancy_smem(g.ka, g.kb, p.mode, m.dense, m.ept, 256,
                                                            p.l.smem)));
     p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(m.items, int64_t{occ} * sms)));
@@ -798,7 +883,7 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     p.a_align = m.sh ? 16 : std::min(16, g.eA * m.va);
     p.b_align = m.sh ? 16 : std::min(16, g.eB * m.vb);
   }
-  p.l.block = 256;
+  if (!(s.v == kSmem && p.sp.dense == 5)) p.l.block = 256;
   *out = p;
   return true;
 }

@@ -23,20 +23,38 @@ struct TileBox {
   uint32_t x0, y0, nx, ny, o;
 };
 
-__device__ __forceinline__ TileBox tile_box(const SmemParams& P, uint32_t it) {
-  TileBox t;
-  uint32_t xc, yc;
+// tile index -> (X chunk, Y chunk, outer index) in the plan's tile order:
+// 0 X chunks fastest, 1 Y chunks fastest, >= 2 groups of P.grp Y chunks
+// (Y fastest inside a group, then X, then the next group)
+__device__ __forceinline__ void smem_tile_coords(const SmemParams& P, uint32_t it, uint32_t& xc,
+                                                 uint32_t& yc, uint32_t& o) {
   if (P.order == 0) {
     const uint32_t q = udiv(it, P.dnx);
     xc = it - q * P.nxc;
-    t.o = udiv(q, P.dny);
-    yc = q - t.o * P.nyc;
-  } else {
+    o = udiv(q, P.dny);
+    yc = q - o * P.nyc;
+  } else if (P.order == 1) {
     const uint32_t q = udiv(it, P.dny);
     yc = it - q * P.nyc;
-    t.o = udiv(q, P.dnx);
-    xc = q - t.o * P.nxc;
+    o = udiv(q, P.dnx);
+    xc = q - o * P.nxc;
+  } else {
+    o = udiv(it, P.dplane);
+    const uint32_t r = it - o * (P.nxc * P.nyc);
+    const uint32_t g = udiv(r, P.dgrp);
+    const uint32_t rr = r - g * (P.grp * P.nxc);
+    const uint32_t y0 = g * P.grp;
+    const uint32_t gh = min(P.grp, P.nyc - y0);
+    const uint32_t q = gh == P.grp ? udiv(rr, P.dG) : rr / gh;
+    xc = q;
+    yc = y0 + (rr - q * gh);
   }
+}
+
+__device__ __forceinline__ TileBox tile_box(const SmemParams& P, uint32_t it) {
+  TileBox t;
+  uint32_t xc, yc;
+  smem_tile_coords(P, it, xc, yc, t.o);
   t.x0 = xc * P.tx;
   t.y0 = yc * P.ty;
   t.nx = min(P.tx, P.X.total - t.x0);

@@ -1,7 +1,8 @@
 // btile.cuh -- the staged tile fed by the Blackwell bulk-copy (TMA) engine.
 //
-// Same tile as dense_kernel / vtile_kernel (S == 1, X group contiguous in A,
-// Y group contiguous in B -- ttune's run_case2, executor.cpp:213-281), but the
+// Same tile as dense_kernel / vtile_kernel (X group contiguous in A, Y group
+// contiguous in B -- ttune's run_case2, executor.cpp:213-281; with a shared
+// stride-1 extent S > 1 the tile is S x tx x ty, run_case1 at 172-211), but the
 // global -> shared side is one cp.async.bulk per tile row instead of one
 // LDGSTS per element or 16-byte chunk, and the kernel is warp specialised:
 //
@@ -100,9 +101,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // (stage layout: btile_stage_bytes, params.hpp)
 
-// P.ns stages, P.pa / P.pb row / column pitches (bytes), P.ly lanes along y
-// (power of two <= 32; 32 / ly columns per warp step), JY = tile rows per lane
-// (ty <= JY * ly).  MODE 0/1/2 as Update.
+// P.ns stages, P.pa / P.pb row / column pitches (bytes), P.ly lanes along a
+// tile column (power of two <= 32; 32 / ly columns per warp step), JY = column
+// elements per lane (S*ty <= JY * ly).  P.S is the shared stride-1 extent (1
+// when A's and B's stride-1 indices differ): an A tile row is then S*tx
+// elements, a B tile column S*ty.  MODE 0/1/2 as Update.
 // EXP (kernel-design probes only, scripts/btile_probe.cu): bit 0 skips the B
 // stores, bit 1 skips the bulk copies (the ring still cycles), bit 2 skips the
 // consumers' work (they only wait and release)
@@ -155,9 +158,9 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
       for (uint32_t y = pl; y < t.ny; y += 32 * PW) {
         int64_t a, b;
         decode(P.Y, t.y0 + y, a, b);
-        const uint64_t start = reinterpret_cast<uint64_t>(A + (a + aO + t.x0) * EA);
+        const uint64_t start = reinterpret_cast<uint64_t>(A + (a + aO + t.x0 * P.S) * EA);
         const uint64_t lo = start & ~uint64_t{15};
-        const uint64_t hi = (start + t.nx * EA + 15) & ~uint64_t{15};
+        const uint64_t hi = (start + t.nx * P.S * EA + 15) & ~uint64_t{15};
         const uint32_t n = static_cast<uint32_t>(hi - lo);
         if constexpr (!(EXP & 2)) {
           bulk_g2s(ta + y * P.pa, reinterpret_cast<const void*>(lo), n, &full[s]);
@@ -168,12 +171,12 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
       for (uint32_t x = pl; x < t.nx; x += 32 * PW) {
         int64_t a, b;
         decode(P.X, t.x0 + x, a, b);
-        const int64_t bo = b + bO + t.y0;
+        const int64_t bo = b + bO + t.y0 * P.S;
         boff[x] = static_cast<uint32_t>(bo);
         if constexpr (UPD) {
           const uint64_t start = reinterpret_cast<uint64_t>(Bc + bo * EB);
           const uint64_t lo = start & ~uint64_t{15};
-          const uint64_t hi = (start + t.ny * EB + 15) & ~uint64_t{15};
+          const uint64_t hi = (start + t.ny * P.S * EB + 15) & ~uint64_t{15};
           const uint32_t n = static_cast<uint32_t>(hi - lo);
           bulk_g2s(tb + x * P.pb, reinterpret_cast<const void*>(lo), n, &full[s]);
           bytes += n;
@@ -205,15 +208,19 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
     const uint32_t* cbase = boff + P.tx;
     const E* ta = reinterpret_cast<const E*>(st + tables);
     const EBv* tb = reinterpret_cast<const EBv*>(st + tables + P.ty * P.pa);
-    // this lane's JY tile rows (y = yi + j*ly) are fixed for the tile; UX
-    // columns per step, all loads of a step issued before its stores
+    // a tile column is S*ny elements contiguous in B (element e = y*S + s);
+    // this lane's JY column elements (e = yi + j*ly) are fixed for the tile,
+    // rb[j] = where element e of column 0 sits in the A tile; UX columns per
+    // step, all loads of a step issued before its stores
+    const uint32_t L = t.ny * P.S;
     uint32_t rb[JY];
     bool yv[JY];
 #pragma unroll
     for (int j = 0; j < JY; ++j) {
-      const uint32_t y = yi + j * ly;
-      yv[j] = y < t.ny;
-      rb[j] = yv[j] ? rbase[y] : 0u;
+      const uint32_t e = yi + j * ly;
+      yv[j] = e < L;
+      const uint32_t y = P.S == 1 ? e : udiv(e, P.dS);
+      rb[j] = yv[j] ? rbase[y] + (e - y * P.S) : 0u;
     }
     for (uint32_t x0 = warp * lxn + xi; x0 < ((EXP & 4) ? 0u : t.nx); x0 += UX * xstep) {
       EBv* q[UX];
@@ -232,7 +239,7 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
       for (int u = 0; u < UX; ++u)
 #pragma unroll
         for (int j = 0; j < JY; ++j) {
-          const E a = ta[rb[j] + xs[u]];
+          const E a = ta[rb[j] + xs[u] * P.S];
           if constexpr (UPD) {
             const EBv b = tb[cb[u] + (yv[j] ? yi + j * ly : 0u)];  // stay inside the column
 #pragma unroll

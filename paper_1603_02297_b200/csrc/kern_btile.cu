@@ -1,7 +1,7 @@
 // kern_btile.cu -- instantiation and launch of btile_kernel (btile.cuh): the
 // four same-kind pairs (mixed pairs run on the other staged tiles), update
-// modes 0/1/2 (beta != 0 always stages B through the bulk-copy ring), 1/2/4/8
-// tile rows per consumer lane.
+// modes 0/1/2 (beta != 0 always stages B through the bulk-copy ring), 1-16
+// column elements per consumer lane.
 #include <type_traits>
 
 #include "btile.cuh"
@@ -29,6 +29,7 @@ cudaError_t with_btile(int ka, int kb, int mode, int jy, F&& f) {
           case 2: return f(&btile_kernel<SA, SA, T::C, M, 2>);
           case 4: return f(&btile_kernel<SA, SA, T::C, M, 4>);
           case 8: return f(&btile_kernel<SA, SA, T::C, M, 8>);
+          case 16: return f(&btile_kernel<SA, SA, T::C, M, 16>);
           default: return cudaErrorInvalidValue;
         }
       });
@@ -39,7 +40,7 @@ cudaError_t with_btile(int ka, int kb, int mode, int jy, F&& f) {
 
 cudaError_t launch_btile(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                          cudaStream_t s) {
-  return with_btile(ka, kb, mode, btile_rows_per_lane(p.ty, p.ly), [&](auto fn) {
+  return with_btile(ka, kb, mode, btile_rows_per_lane(p.S * p.ty, p.ly), [&](auto fn) {
     if (l.smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
       if (e != cudaSuccess) return e;

@@ -140,10 +140,10 @@ TTB_HD uint32_t btile_stage_bytes(uint32_t tx, uint32_t ty, uint32_t pa, uint32_
   return btile_tables_bytes(tx, ty, upd) + ty * pa + (upd ? tx * pb : 0u);
 }
 
-// btile_kernel tile rows per consumer lane (template JY: 1, 2, 4 or 8)
-TTB_HD int btile_rows_per_lane(uint32_t ty, uint32_t ly) {
-  const uint32_t n = (ty + ly - 1) / ly;
-  return n <= 1 ? 1 : n <= 2 ? 2 : n <= 4 ? 4 : 8;
+// btile_kernel column elements per consumer lane (template JY: 1, 2, 4, 8 or 16)
+TTB_HD int btile_rows_per_lane(uint32_t col, uint32_t ly) {  // col = S*ty
+  const uint32_t n = (col + ly - 1) / ly;
+  return n <= 1 ? 1 : n <= 2 ? 2 : n <= 4 ? 4 : n <= 8 ? 8 : 16;
 }
 
 // Launch shape chosen by the planner.

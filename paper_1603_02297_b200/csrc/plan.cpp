@@ -162,8 +162,8 @@ uint32_t best_row_length(uint32_t S, uint32_t tx, uint32_t ty, int ebytes) {
   return best;
 }
 
-bool x_dense_in_a(const Geo& g, const std::vector<int>& xs);
-bool y_dense_in_b(const Geo& g, const std::vector<int>& ys);
+bool x_dense_in_a(const Geo& g, const std::vector<int>& xs, int64_t lead = 1);
+bool y_dense_in_b(const Geo& g, const std::vector<int>& ys, int64_t lead = 1);
 
 // vector widths of vtile_kernel for a tile (false: element-wise only)
 bool vtile_widths(const Geo& g, const std::vector<int>& xs, const std::vector<int>& ys, int64_t tx,
@@ -236,15 +236,17 @@ int64_t pow2_ceil(int64_t v) {
   return p;
 }
 
-bool x_dense_in_a(const Geo& g, const std::vector<int>& xs) {
-  if (xs.empty() || g.sa[xs[0]] != 1) return false;
+// X group contiguous in A right after `lead` elements (the shared stride-1
+// extent, 1 when the stride-1 index is transposed)
+bool x_dense_in_a(const Geo& g, const std::vector<int>& xs, int64_t lead) {
+  if (xs.empty() || g.sa[xs[0]] != lead) return false;
   for (size_t i = 0; i + 1 < xs.size(); ++i)
     if (g.sa[xs[i + 1]] != g.sa[xs[i]] * g.n[xs[i]]) return false;
   return true;
 }
 
-bool y_dense_in_b(const Geo& g, const std::vector<int>& ys) {
-  if (ys.empty() || g.sb[ys[0]] != 1) return false;
+bool y_dense_in_b(const Geo& g, const std::vector<int>& ys, int64_t lead) {
+  if (ys.empty() || g.sb[ys[0]] != lead) return false;
   for (size_t i = 0; i + 1 < ys.size(); ++i)
     if (g.sb[ys[i + 1]] != g.sb[ys[i]] * g.n[ys[i]]) return false;
   return true;
@@ -283,26 +285,26 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
       std::vector<int64_t> txs, tys;
       sides(NX, &txs);
       sides(NY, &tys);
-      if (!shared && fast && g.ka == g.kb && x_dense_in_a(g, xs) && y_dense_in_b(g, ys)) {
-        // bulk-copy tiles (btile.cuh): sides 32..256 (or the whole group),
-        // 8-64 KB of tile, as many ring stages as fit one or two CTAs per SM
-        auto bsides = [](int64_t N) {
+      if (fast && g.ka == g.kb && x_dense_in_a(g, xs, S) && y_dense_in_b(g, ys, S)) {
+        // bulk-copy tiles (btile.cuh): A rows of S*tx and B columns of S*ty
+        // elements (S*ty <= 512), 8-64 KB of tile, 2-3 ring stages
+        auto bsides = [](int64_t N, int64_t cap) {
           std::vector<int64_t> v;
-          for (int64_t t : {32, 64, 128, 256})
-            if (t < N) v.push_back(t);
-          if (N <= 256) v.push_back(N);
+          for (int64_t t : {1, 2, 4, 8, 16, 32, 64, 128, 256})
+            if (t < N && t <= cap) v.push_back(t);
+          if (N <= cap) v.push_back(N);
           return v;
         };
-        for (int64_t tx : bsides(NX)) {
-          for (int64_t ty : bsides(NY)) {
-            const int64_t bytes = tx * ty * std::max(g.eA, g.eB);
+        for (int64_t tx : bsides(NX, 256)) {
+          for (int64_t ty : bsides(NY, std::min<int64_t>(256, 512 / S))) {
+            const int64_t bytes = S * tx * ty * std::max(g.eA, g.eB);
             if (bytes > 64 * 1024 || (bytes < 8 * 1024 && !(tx >= NX && ty >= NY))) continue;
             const double ex = static_cast<double>(NX) / (((NX + tx - 1) / tx) * tx);
             const double ey = static_cast<double>(NY) / (((NY + ty - 1) / ty) * ty);
-            const int64_t run_a = tx * g.eA, run_b = ty * g.eB;
+            const int64_t run_a = S * tx * g.eA, run_b = S * ty * g.eB;
             auto run_cost = [](int64_t r) { return r < 64 ? 4.0 : r < 128 ? 1.5 : r < 256 ? 0.5 : 0.0; };
-            const int64_t stage = (tx + ty * 2) * 4 + ty * (tx * g.eA + 32) +
-                                  (g.mode == 2 ? tx * (ty * g.eB + 16) : 0);
+            const int64_t stage = (tx * 2 + ty) * 4 + ty * (S * tx * g.eA + 32) +
+                                  (g.mode == 2 ? tx * (S * ty * g.eB + 32) : 0);
             // a CTA keeps about one stage of bulk copies moving at a time, so
             // throughput comes from 3-6 CTAs per SM with 2-3 stages each
             for (int64_t ns : {int64_t{3}, int64_t{2}}) {
@@ -804,23 +806,23 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     if (s.vec == 3) {
       // bulk-copy tile (btile.cuh): one cp.async.bulk per A row (and B column
       // when beta != 0), any element alignment, warp-specialised ring
-      if (!(small && m.S == 1 && g.ka == g.kb && x_dense_in_a(g, xs) && y_dense_in_b(g, ys)))
+      if (!(small && g.ka == g.kb && x_dense_in_a(g, xs, m.S) && y_dense_in_b(g, ys, m.S)))
         return fail("smem: bulk tile needs equal kinds, contiguous X in A and Y in B");
-      if (m.tx > 256 || m.ty > 256) return fail("smem: bulk tile side above 256");
+      if (m.tx > 256 || m.ty > 256 || m.S * m.ty > 512) return fail("smem: bulk tile too large");
       if (s.st < 2 || s.st > 8) return fail("smem: bulk tile stages outside 2..8");
       m.dense = 5;
       m.ept = 0;
       m.ly = 1;
-      while (m.ly < 32 && m.ly < m.ty) m.ly *= 2;
+      while (m.ly < 32 && m.ly < m.S * m.ty) m.ly *= 2;
       // a row's 16-byte superset spans at most tx*e + 16 - e bytes; an odd
       // number of 16-byte units keeps 8 consecutive rows on distinct banks
       auto pitch = [](uint32_t n, int e) {
         uint32_t b = (n * static_cast<uint32_t>(e) + 16u - static_cast<uint32_t>(std::min(e, 16)) + 15u) & ~15u;
         return b;
       };
-      m.pa = pitch(m.tx, g.eA);
+      m.pa = pitch(m.S * m.tx, g.eA);
       if ((m.pa / 16) % 2 == 0) m.pa += 16;
-      m.pb = pitch(m.ty, g.eB);
+      m.pb = pitch(m.S * m.ty, g.eB);
       m.ns = static_cast<uint32_t>(s.st);
     } else if (s.vec == 2) {
       if (!(s.st == 2 && small && m.S == 1 && vtile_shift(g, xs, ys, m.tx, m.ty, &va, &sh)))
@@ -873,7 +875,7 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
       p.l.block = 32 * 6;  // kBtileConsumerWarps + kBtileProducerWarps (btile.cuh)
     }
     const int occ = std::min(
-        occ_cap, std::max(1, m.dense == 5 ? occupancy_btile(g.ka, g.kb, p.mode, btile_rows_per_lane(m.ty, m.ly), p.l.block, p.l.smem) :
+        occ_cap, std::max(1, m.dense == 5 ? occupancy_btile(g.ka, g.kb, p.mode, btile_rows_per_lane(m.S * m.ty, m.ly), p.l.block, p.l.smem) :
                              m.dense == 4 ? occupancy_vtile(g.ka, g.kb, p.mode, m.va, m.vb, m.sh, 256, p.l.smem)
                                           : occupancy_smem(g.ka, g.kb, p.mode, m.dense, m.ept, 256,
                                                            p.l.smem)));

@@ -737,7 +737,7 @@ int ttb_plan_describe(ttb_plan plan, char* buf, size_t len) {
   // the plan text plus the kernel that runs it (informational "fn" key)
   const Prepared& p = plan->prep;
   const char* fn = p.spec.v == kRt ? "rt" : p.spec.v == kCopy ? (p.cp.long_rows ? "copy_rows" : "copy")
-                   : p.sp.dense == 5 ? "btile" : p.sp.dense == 4 ? "vtile" : p.sp.dense >= 2 ? "dense" : p.sp.dense == 1 ? "tile" : "smem";
+                   : p.sp.dense == 5 ? (p.sp.ly ? "btile" : "btile_lin") : p.sp.dense == 4 ? "vtile" : p.sp.dense >= 2 ? "dense" : p.sp.dense == 1 ? "tile" : "smem";
   const std::string t = p.spec.text() + ";fn=" + fn;
   if (!buf || len <= t.size()) return fail(TTB_EINVAL, "describe: buffer too small");
   std::memcpy(buf, t.c_str(), t.size() + 1);

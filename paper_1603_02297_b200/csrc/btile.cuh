@@ -103,9 +103,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // P.ns stages, P.pa / P.pb row / column pitches (bytes), P.ly lanes along a
 // tile column (power of two <= 32; 32 / ly columns per warp step), JY = column
-// elements per lane (S*ty <= JY * ly).  P.S is the shared stride-1 extent (1
+// elements per lane (S*ty <= JY * ly; JY == 0: the linear walk, any S*ty,
+// P.ly == 0).  P.S is the shared stride-1 extent (1
 // when A's and B's stride-1 indices differ): an A tile row is then S*tx
-// elements, a B tile column S*ty.  MODE 0/1/2 as Update.
+// elements, a B tile column S*ty.  MODE 0-3 as Update (3: B read directly
+// by the consumers, not through the ring).
 // EXP (kernel-design probes only, scripts/btile_probe.cu): bit 0 skips the B
 // stores, bit 1 skips the bulk copies (the ring still cycles), bit 2 skips the
 // consumers' work (they only wait and release)
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
   using E = Vec<SA, C>;
   using EBv = Vec<SB, C>;
   constexpr uint32_t EA = sizeof(E), EB = sizeof(EBv);
-  constexpr bool UPD = MODE == 2;
+  constexpr bool UPD = MODE == 2;  // B staged through the ring (MODE 3 reads B directly)
   // columns per consumer step: ~4 words of loads in flight per tile row
   constexpr int UX = EB <= 4 ? 4 : EB <= 8 ? 2 : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -154,33 +156,82 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
       unsigned char* ta = st + tables;
       unsigned char* tb = ta + P.ty * P.pa;
       uint32_t bytes = 0;
-      const uint32_t pl = (warp - NC) * 32 + lane;  // producer lane
-      for (uint32_t y = pl; y < t.ny; y += 32 * PW) {
-        int64_t a, b;
-        decode(P.Y, t.y0 + y, a, b);
-        const uint64_t start = reinterpret_cast<uint64_t>(A + (a + aO + t.x0 * P.S) * EA);
-        const uint64_t lo = start & ~uint64_t{15};
-        const uint64_t hi = (start + t.nx * P.S * EA + 15) & ~uint64_t{15};
-        const uint32_t n = static_cast<uint32_t>(hi - lo);
-        if constexpr (!(EXP & 2)) {
-          bulk_g2s(ta + y * P.pa, reinterpret_cast<const void*>(lo), n, &full[s]);
-          bytes += n;
+      // P.runs bit 0 / 1: A rows / B columns may continue each other (the
+      // planner's static test); then items are handled 32 at a time per warp:
+      // whose data continue each other in memory (a row right after the
+      // previous row: the tile spans X completely and Y's first axis follows
+      // X in A; likewise for B columns) are fetched as one bulk copy per run,
+      // landing packed from the run's first slot; tab[i] = element index of
+      // item i's first element in the region.
+      auto fetch = [&](uint32_t base, uint32_t cnt, uint32_t len, int64_t off, const unsigned char* gbase,
+                       uint32_t esz, unsigned char* region, uint32_t pitch, uint32_t* tab) {
+        const uint32_t i = base + lane;
+        const bool valid = i < cnt;
+        const int64_t prev = __shfl_up_sync(0xffffffffu, off, 1);
+        const bool start = valid && (lane == 0 || prev + len != off);
+        const uint32_t smask = __ballot_sync(0xffffffffu, start);
+        const uint32_t nvalid = __popc(__ballot_sync(0xffffffffu, valid));
+        uint32_t shift = 0;
+        if (start) {
+          const uint32_t above = smask & ~((2u << lane) - 1u);
+          const uint32_t end = min(above ? static_cast<uint32_t>(__ffs(above)) - 1u : 32u, nvalid);
+          const uint64_t ga = reinterpret_cast<uint64_t>(gbase + off * esz);
+          const uint64_t lo = ga & ~uint64_t{15};
+          const uint64_t hi = (ga + static_cast<uint64_t>(end - lane) * len * esz + 15) & ~uint64_t{15};
+          shift = static_cast<uint32_t>(ga - lo);
+          if constexpr (!(EXP & 2)) {
+            bulk_g2s(region + i * pitch, reinterpret_cast<const void*>(lo), static_cast<uint32_t>(hi - lo),
+                     &full[s]);
+            bytes += static_cast<uint32_t>(hi - lo);
+          }
         }
-        rbase[y] = (y * P.pa + static_cast<uint32_t>(start - lo)) / EA;
+        const uint32_t s0 = valid ? 31u - __clz(smask & ((2u << lane) - 1u)) : 0u;
+        const uint32_t sh0 = __shfl_sync(0xffffffffu, shift, s0);
+        if (valid) tab[i] = ((base + s0) * pitch + sh0) / esz + (lane - s0) * len;
+      };
+      // one bulk copy per item (the common case: no item continues another)
+      auto fetch1 = [&](uint32_t i, uint32_t len, int64_t off, const unsigned char* gbase, uint32_t esz,
+                        unsigned char* region, uint32_t pitch, uint32_t* tab) {
+        const uint64_t ga = reinterpret_cast<uint64_t>(gbase + off * esz);
+        const uint64_t lo = ga & ~uint64_t{15};
+        const uint64_t hi = (ga + static_cast<uint64_t>(len) * esz + 15) & ~uint64_t{15};
+        if constexpr (!(EXP & 2)) {
+          bulk_g2s(region + i * pitch, reinterpret_cast<const void*>(lo), static_cast<uint32_t>(hi - lo),
+                   &full[s]);
+          bytes += static_cast<uint32_t>(hi - lo);
+        }
+        tab[i] = (i * pitch + static_cast<uint32_t>(ga - lo)) / esz;
+      };
+      if (P.runs & 1) {
+        for (uint32_t base = (warp - NC) * 32; base < t.ny; base += 32 * PW) {
+          int64_t a = 0, b;
+          const uint32_t y = base + lane;
+          if (y < t.ny) decode(P.Y, t.y0 + y, a, b);
+          fetch(base, t.ny, t.nx * P.S, a + aO + t.x0 * P.S, A, EA, ta, P.pa, rbase);
+        }
+      } else {
+        for (uint32_t y = (warp - NC) * 32 + lane; y < t.ny; y += 32 * PW) {
+          int64_t a, b;
+          decode(P.Y, t.y0 + y, a, b);
+          fetch1(y, t.nx * P.S, a + aO + t.x0 * P.S, A, EA, ta, P.pa, rbase);
+        }
       }
-      for (uint32_t x = pl; x < t.nx; x += 32 * PW) {
-        int64_t a, b;
-        decode(P.X, t.x0 + x, a, b);
-        const int64_t bo = b + bO + t.y0 * P.S;
-        boff[x] = static_cast<uint32_t>(bo);
-        if constexpr (UPD) {
-          const uint64_t start = reinterpret_cast<uint64_t>(Bc + bo * EB);
-          const uint64_t lo = start & ~uint64_t{15};
-          const uint64_t hi = (start + t.ny * P.S * EB + 15) & ~uint64_t{15};
-          const uint32_t n = static_cast<uint32_t>(hi - lo);
-          bulk_g2s(tb + x * P.pb, reinterpret_cast<const void*>(lo), n, &full[s]);
-          bytes += n;
-          cbase[x] = (x * P.pb + static_cast<uint32_t>(start - lo)) / EB;
+      if (UPD && (P.runs & 2)) {
+        for (uint32_t base = (warp - NC) * 32; base < t.nx; base += 32 * PW) {
+          int64_t a, b = 0;
+          const uint32_t x = base + lane;
+          if (x < t.nx) decode(P.X, t.x0 + x, a, b);
+          const int64_t bo = b + bO + t.y0 * P.S;
+          if (x < t.nx) boff[x] = static_cast<uint32_t>(bo);
+          fetch(base, t.nx, t.ny * P.S, bo, Bc, EB, tb, P.pb, cbase);
+        }
+      } else {
+        for (uint32_t x = (warp - NC) * 32 + lane; x < t.nx; x += 32 * PW) {
+          int64_t a, b;
+          decode(P.X, t.x0 + x, a, b);
+          const int64_t bo = b + bO + t.y0 * P.S;
+          boff[x] = static_cast<uint32_t>(bo);
+          if constexpr (UPD) fetch1(x, t.ny * P.S, bo, Bc, EB, tb, P.pb, cbase);
         }
       }
       mbar_arrive_expect_tx(&full[s], bytes);
@@ -208,6 +259,38 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
     const uint32_t* cbase = boff + P.tx;
     const E* ta = reinterpret_cast<const E*>(st + tables);
     const EBv* tb = reinterpret_cast<const EBv*>(st + tables + P.ty * P.pa);
+    if constexpr (JY == 0) {
+      // linear walk of the tile in B order: element e of the tile index space
+      // is column x = e / (S*ty), element c = e mod (S*ty) of that column; the
+      // lanes of a warp cover consecutive B addresses even when a column is
+      // shorter than a warp (small ty, or a column run that continues into
+      // the next column)
+      const uint32_t Lf = P.S * P.ty, Lv = P.S * t.ny, total = Lf * t.nx;
+      constexpr int U = 4;
+      for (uint32_t e0 = warp * 32 + lane; e0 < ((EXP & 4) ? 0u : total); e0 += U * 32 * NC) {
+        EBv w[U];
+        EBv* q[U];
+        bool v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t e = e0 + u * 32 * NC;
+          const uint32_t x = udiv(e, P.dcol);
+          const uint32_t c = e - x * Lf;
+          v[u] = e < total && c < Lv;
+          const uint32_t xc = v[u] ? x : 0u, cc = v[u] ? c : 0u;
+          const uint32_t y = P.S == 1 ? cc : udiv(cc, P.dS);
+          const E a = ta[rbase[y] + xc * P.S + (cc - y * P.S)];
+          q[u] = B + boff[xc] + cc;
+          EBv b;
+          if constexpr (UPD) b = tb[cbase[xc] + cc];
+          if constexpr (MODE == 3) vload_b_pred(b, q[u]->v, v[u]);
+#pragma unroll
+          for (int k = 0; k < C; ++k) w[u].v[k] = up(a.v[k], MODE >= 2 ? b.v[k] : SB(0));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) vstore_pred(q[u]->v, w[u], v[u]);
+      }
+    } else {
     // a tile column is S*ny elements contiguous in B (element e = y*S + s);
     // this lane's JY column elements (e = yi + j*ly) are fixed for the tile,
     // rb[j] = where element e of column 0 sits in the A tile; UX columns per
@@ -244,6 +327,11 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
             const EBv b = tb[cb[u] + (yv[j] ? yi + j * ly : 0u)];  // stay inside the column
 #pragma unroll
             for (int c = 0; c < C; ++c) w[u][j].v[c] = up(a.v[c], b.v[c]);
+          } else if constexpr (MODE == 3) {
+            EBv b;
+            vload_b_pred(b, q[u][j * ly].v, xv[u] && yv[j]);
+#pragma unroll
+            for (int c = 0; c < C; ++c) w[u][j].v[c] = up(a.v[c], b.v[c]);
           } else {
 #pragma unroll
             for (int c = 0; c < C; ++c) w[u][j].v[c] = up(a.v[c], SB(0));
@@ -259,6 +347,7 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
             vstore_pred(q[u][j * ly].v, w[u][j], xv[u] && yv[j]);
           }
         }
+    }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);

@@ -125,6 +125,8 @@ struct SmemParams {
   // B columns continue across tiles (longer DRAM runs on both sides)
   uint32_t grp;
   Div32 dplane, dgrp, dG;  // nxc*nyc, grp*nxc, grp
+  Div32 dcol;              // dense == 5, linear walk: S*ty (tile column length)
+  int runs;                // dense == 5: bit 0 A tile rows / bit 1 B tile columns may be contiguous
 };
 
 // btile_kernel shared-memory layout of one stage (all offsets 16-byte aligned):

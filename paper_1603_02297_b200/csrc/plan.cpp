@@ -295,33 +295,48 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
           if (N <= cap) v.push_back(N);
           return v;
         };
-        for (int64_t tx : bsides(NX, 256)) {
-          for (int64_t ty : bsides(NY, std::min<int64_t>(256, 512 / S))) {
+        for (int64_t tx : bsides(NX, 1024)) {
+          for (int64_t ty : bsides(NY, 1024)) {
             const int64_t bytes = S * tx * ty * std::max(g.eA, g.eB);
-            if (bytes > 64 * 1024 || (bytes < 8 * 1024 && !(tx >= NX && ty >= NY))) continue;
+            if (bytes > 64 * 1024 || (bytes < 4 * 1024 && !(tx >= NX && ty >= NY))) continue;
             const double ex = static_cast<double>(NX) / (((NX + tx - 1) / tx) * tx);
             const double ey = static_cast<double>(NY) / (((NY + ty - 1) / ty) * ty);
-            const int64_t run_a = S * tx * g.eA, run_b = S * ty * g.eB;
+            // a B column that covers its whole group continues into the next
+            // column when X's first axis is B's next position
+            int64_t run_a = S * tx * g.eA, run_b = S * ty * g.eB;
+            if (ty >= NY && g.sb[xs[0]] == S * NY) run_b *= std::min<int64_t>(tx, g.n[xs[0]]);
+            if (tx >= NX && g.sa[ys[0]] == S * NX) run_a *= std::min<int64_t>(ty, g.n[ys[0]]);
             auto run_cost = [](int64_t r) { return r < 64 ? 4.0 : r < 128 ? 1.5 : r < 256 ? 0.5 : 0.0; };
-            const int64_t stage = (tx * 2 + ty) * 4 + ty * (S * tx * g.eA + 32) +
-                                  (g.mode == 2 ? tx * (S * ty * g.eB + 32) : 0);
-            // a CTA keeps about one stage of bulk copies moving at a time, so
-            // throughput comes from 3-6 CTAs per SM with 2-3 stages each
-            for (int64_t ns : {int64_t{3}, int64_t{2}}) {
-              if (ns * stage > 110 * 1024) continue;
-              const int64_t budget = ns == 3 ? 200 * 1024 : 100 * 1024;
-              Spec b;
-              b.v = kSmem;
-              b.kx = kx;
-              b.ky = ky;
-              b.tx = static_cast<int>(tx);
-              b.ty = static_cast<int>(ty);
-              b.vec = 3;
-              b.st = static_cast<int>(ns);
-              b.cost = 1.0 + (1.0 - ex * ey) * 12.0 + run_cost(run_a) + run_cost(run_b) +
-                       std::fabs(std::log2(static_cast<double>(bytes) / 16384.0)) * 0.2 +
-                       0.05 * (kx + ky) + (budget < 200 * 1024 ? 0.02 : 0.0);
-              bulk->push_back(b);
+            for (int lin = 0; lin < 2; ++lin) {
+              // column walk: lanes along a column (S*ty <= 512, sides <= 256);
+              // linear walk: lanes along the tile in B order (any shape)
+              if (!lin && (S * ty > 512 || tx > 256 || ty > 256)) continue;
+              const double lanes = lin ? 1.0 : std::min(1.0, static_cast<double>(S * ty) / 32.0);
+              for (int bp = 1; bp >= (g.mode == 2 ? 0 : 1); --bp) {
+                const int64_t stage = (tx * 2 + ty) * 4 + ty * (S * tx * g.eA + 32) +
+                                      (g.mode == 2 && bp ? tx * (S * ty * g.eB + 32) : 0);
+                // a CTA keeps about one stage of bulk copies moving at a time, so
+                // throughput comes from 3-6 CTAs per SM with 2-3 stages each
+                for (int64_t ns : {int64_t{3}, int64_t{2}}) {
+                  if (ns * stage > 110 * 1024) continue;
+                  Spec b;
+                  b.v = kSmem;
+                  b.kx = kx;
+                  b.ky = ky;
+                  b.tx = static_cast<int>(tx);
+                  b.ty = static_cast<int>(ty);
+                  b.vec = lin ? 4 : 3;
+                  b.bp = bp;
+                  b.st = static_cast<int>(ns);
+                  // B columns of fewer than 128 bytes make many tiny bulk copies
+                  const double small_cols = (g.mode == 2 && bp && S * ty * g.eB < 128) ? 2.0 : 0.0;
+                  b.cost = 1.0 + (1.0 - ex * ey) * 12.0 + run_cost(run_a) + run_cost(run_b) +
+                           std::fabs(std::log2(static_cast<double>(bytes) / 16384.0)) * 0.2 +
+                           0.05 * (kx + ky) + (ns == 2 ? 0.02 : 0.0) + (1.0 - lanes) * 3.0 +
+                           (lin ? 0.3 : 0.0) + small_cols + (bp ? 0.0 : 0.1);
+                  bulk->push_back(b);
+                }
+              }
             }
           }
         }
@@ -372,7 +387,33 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
                    [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
   std::stable_sort(bulk_specs.begin(), bulk_specs.end(),
                    [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
-  for (size_t i = 0; i < bulk_specs.size() && i < 6; ++i) out->push_back(bulk_specs[i]);
+  // the cheapest few by the heuristic, plus the square-ish tiles that measure
+  // best on most shapes (the waste term over-penalises their partial tiles),
+  // the best linear-walk tiles and the best direct-B (bp=0) tiles
+  {
+    std::vector<Spec> pick;
+    auto add = [&](const Spec& b) {
+      for (const Spec& q : pick)
+        if (q.text() == b.text()) return false;
+      pick.push_back(b);
+      return true;
+    };
+    for (size_t i = 0; i < bulk_specs.size() && pick.size() < 4; ++i) add(bulk_specs[i]);
+    int n = 0;
+    for (const Spec& b : bulk_specs) {
+      const int64_t el = static_cast<int64_t>(S) * b.tx * b.ty;
+      const bool squareish = b.vec == 3 && b.bp == 1 && b.st == 2 && el >= 2048 && el <= 8192 &&
+                             b.tx >= 16 && static_cast<int64_t>(S) * b.ty >= 16;
+      if (squareish && n < 4 && add(b)) ++n;
+    }
+    n = 0;
+    for (const Spec& b : bulk_specs)
+      if (b.vec == 4 && n < 2 && add(b)) ++n;
+    n = 0;
+    for (const Spec& b : bulk_specs)
+      if (b.bp == 0 && n < 2 && add(b)) ++n;
+    for (const Spec& b : pick) out->push_back(b);
+  }
   for (size_t i = 0; i < cand.size() && i < 8; ++i) {
     out->push_back(cand[i]);
     int va, vb;
@@ -613,7 +654,7 @@ std::vector<Spec> candidates(const Geo& g) {
   int n_bulk = 0, n_other = 0;
   for (size_t i = 0; i < out.size(); ++i)
     if (out[i].v != kCopy) {
-      int& n = (out[i].v == kSmem && out[i].vec == 3) ? n_bulk : n_other;
+      int& n = (out[i].v == kSmem && out[i].vec >= 3) ? n_bulk : n_other;
       if (n >= 2) continue;
       ++n;
       Spec s = out[i];
@@ -645,12 +686,12 @@ std::vector<Spec> candidates(const Geo& g) {
     }
   // cap the list but keep every family represented: the best few copy and
   // register-transpose candidates survive even when staged tiles rank higher
-  if (out.size() > 32) {
-    std::vector<Spec> kept(out.begin(), out.begin() + 32);
+  if (out.size() > 40) {
+    std::vector<Spec> kept(out.begin(), out.begin() + 40);
     for (Variant v : {kCopy, kRt}) {
       int have = 0;
       for (const Spec& k : kept) have += k.v == v;
-      for (size_t i = 32; i < out.size() && have < 4; ++i)
+      for (size_t i = 40; i < out.size() && have < 4; ++i)
         if (out[i].v == v) {
           kept.push_back(out[i]);
           ++have;
@@ -802,18 +843,27 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     int va = 1, vb = 1, sh = 0;
     m.sh = 0;
     m.ns = m.pa = m.pb = 0;
+    m.runs = 0;
     m.ly = 32;
-    if (s.vec == 3) {
+    if (s.vec == 3 || s.vec == 4) {
       // bulk-copy tile (btile.cuh): one cp.async.bulk per A row (and B column
       // when beta != 0), any element alignment, warp-specialised ring
       if (!(small && g.ka == g.kb && x_dense_in_a(g, xs, m.S) && y_dense_in_b(g, ys, m.S)))
         return fail("smem: bulk tile needs equal kinds, contiguous X in A and Y in B");
-      if (m.tx > 256 || m.ty > 256 || m.S * m.ty > 512) return fail("smem: bulk tile too large");
+      const bool lin = s.vec == 4;  // linear walk (any column length)
+      if (m.tx > 1024 || m.ty > 1024 || (!lin && (m.tx > 256 || m.ty > 256 || m.S * m.ty > 512)))
+        return fail("smem: bulk tile too large");
       if (s.st < 2 || s.st > 8) return fail("smem: bulk tile stages outside 2..8");
       m.dense = 5;
       m.ept = 0;
       m.ly = 1;
       while (m.ly < 32 && m.ly < m.S * m.ty) m.ly *= 2;
+      if (lin) m.ly = 0;
+      m.dcol = Div32::make(m.S * m.ty);
+      // consecutive tile rows are contiguous in A when the tile spans X and
+      // Y's first axis follows X in A; likewise B columns
+      m.runs = ((m.tx >= m.X.total && g.sa[ys[0]] == static_cast<int64_t>(m.S) * m.X.total) ? 1 : 0) |
+               ((m.ty >= m.Y.total && g.sb[xs[0]] == static_cast<int64_t>(m.S) * m.Y.total) ? 2 : 0);
       // a row's 16-byte superset spans at most tx*e + 16 - e bytes; an odd
       // number of 16-byte units keeps 8 consecutive rows on distinct banks
       auto pitch = [](uint32_t n, int e) {
@@ -860,7 +910,7 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     if (g.mode == 2 && s.bp == 0 && m.dense) p.mode = 3;
     const auto r16 = [](int64_t v) { return (v + 15) & ~int64_t{15}; };
     const int64_t smem =
-        m.dense == 5 ? static_cast<int64_t>(m.ns) * btile_stage_bytes(m.tx, m.ty, m.pa, m.pb, g.mode == 2) :
+        m.dense == 5 ? static_cast<int64_t>(m.ns) * btile_stage_bytes(m.tx, m.ty, m.pa, m.pb, p.mode == 2) :
         m.dense ? (m.dense == 3 ? 3 : 2) *  // pipeline stages (dense_stage_bytes in dense.cuh)
                       (r16(static_cast<int64_t>(m.tx + m.ty) * (m.dense >= 2 ? 4 : 8)) +
                        r16(static_cast<int64_t>(m.ty) * m.rl * g.eA) +
@@ -870,12 +920,9 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
                 : static_cast<int64_t>(m.tx + m.ty) * 2 * 8 + static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);
-    if (m.dense == 5) {
-      p.mode = g.mode;  // beta != 0 always stages B through the ring
-      p.l.block = 32 * 6;  // kBtileConsumerWarps + kBtileProducerWarps (btile.cuh)
-    }
+    if (m.dense == 5) p.l.block = 32 * 6;  // kBtileConsumerWarps + kBtileProducerWarps (btile.cuh)
     const int occ = std::min(
-        occ_cap, std::max(1, m.dense == 5 ? occupancy_btile(g.ka, g.kb, p.mode, btile_rows_per_lane(m.S * m.ty, m.ly), p.l.block, p.l.smem) :
+        occ_cap, std::max(1, m.dense == 5 ? occupancy_btile(g.ka, g.kb, p.mode, m.ly ? btile_rows_per_lane(m.S * m.ty, m.ly) : 0, p.l.block, p.l.smem) :
                              m.dense == 4 ? occupancy_vtile(g.ka, g.kb, p.mode, m.va, m.vb, m.sh, 256, p.l.smem)
                                           : occupancy_smem(g.ka, g.kb, p.mode, m.dense, m.ept, 256,
                                                            p.l.smem)));

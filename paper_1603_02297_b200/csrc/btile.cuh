@@ -35,10 +35,6 @@
 namespace ttb {
 
 constexpr int kBtileMaxStages = 8;
-constexpr int kBtileConsumerWarps = 4;
-// bulk copies are issued per warp through the uniform datapath (one lane's
-// copy at a time), so the issue rate scales with producer warps, not lanes
-constexpr int kBtileProducerWarps = 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

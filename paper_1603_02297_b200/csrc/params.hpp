@@ -129,6 +129,12 @@ struct SmemParams {
   int runs;                // dense == 5: bit 0 A tile rows / bit 1 B tile columns may be contiguous
 };
 
+// btile_kernel warp roles: consumer warps write B; producer warps issue the
+// bulk copies (issued per warp through the uniform datapath, one lane's copy
+// at a time, so the issue rate scales with producer warps, not lanes)
+constexpr int kBtileConsumerWarps = 4;
+constexpr int kBtileProducerWarps = 2;
+
 // btile_kernel shared-memory layout of one stage (all offsets 16-byte aligned):
 //   rbase[ty]  u32: element index of tile row y's first element in the A tile
 //   boff[tx]   u32: B element offset of tile column x's first element

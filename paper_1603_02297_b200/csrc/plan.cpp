@@ -920,7 +920,7 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
                 : static_cast<int64_t>(m.tx + m.ty) * 2 * 8 + static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);
-    if (m.dense == 5) p.l.block = 32 * 6;  // kBtileConsumerWarps + kBtileProducerWarps (btile.cuh)
+    if (m.dense == 5) p.l.block = 32 * (kBtileConsumerWarps + kBtileProducerWarps);
     const int occ = std::min(
         occ_cap, std::max(1, m.dense == 5 ? occupancy_btile(g.ka, g.kb, p.mode, m.ly ? btile_rows_per_lane(m.S * m.ty, m.ly) : 0, p.l.block, p.l.smem) :
                              m.dense == 4 ? occupancy_vtile(g.ka, g.kb, p.mode, m.va, m.vb, m.sh, 256, p.l.smem)

@@ -83,11 +83,13 @@ int main() {
   cudaMalloc(&A, sizeof(float) * N * N);
   cudaMalloc(&B, sizeof(float) * N * N);
   cudaMemset(A, 0, sizeof(float) * N * N);
-  for (int order : {0, 4, 8, 16}) {
-    run<2, 0, 2, 4>(A, B, N, 64, 64, 3, 0, order);
-    run<2, 0, 2, 4>(A, B, N, 128, 64, 2, 0, order);
-    run<1, 0, 2, 4>(A, B, N, 64, 32, 4, 0, order);
-    run<2, 0, 2, 4>(A, B, N, 32, 64, 3, 0, order);
-  }
+  run<2, 0, 2, 4>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 4, 4>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 6, 4>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 4, 2>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 4, 8>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 8, 8>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 4, 4>(A, B, N, 64, 64, 3, 0, 0);
+  run<2, 0, 4, 4>(A, B, N, 128, 64, 2, 0, 0);
   return 0;
 }

@@ -252,7 +252,8 @@ def _strides(ext):
 def variant_of(plan_text):
     """Kernel that runs a plan: the `fn` key of ttb_plan_describe."""
     kv = dict(p.split("=", 1) for p in plan_text.split(";") if "=" in p)
-    return kv.get("fn", kv.get("kern", "?"))
+    fn = kv.get("fn", kv.get("kern", "?"))
+    return "btile" if fn == "btile_lin" else fn  # one kernel, two consumer walks
 
 
 # ------------------------------------------------------------ reference arm --

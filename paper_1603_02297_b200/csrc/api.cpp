@@ -605,15 +605,15 @@ int ttb_plan_autotune(ttb_plan plan, const void* A, void* B, int warmups, int re
       timed.emplace_back(measure(pr, warmups, reps), pr);
       if (rc) break;
     }
-    // second round: the three fastest again, interleaved, so one noisy sample
+    // second round: the four fastest again (three times), interleaved, so one noisy sample
     // cannot decide; ties keep the earlier (heuristically better) candidate,
     // like select_solution's cost tie-break (tuner.cpp:48-64)
     std::vector<size_t> order(timed.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = i;
     std::stable_sort(order.begin(), order.end(),
                      [&](size_t a, size_t b) { return timed[a].first < timed[b].first; });
-    if (order.size() > 3) order.resize(3);
-    for (int round = 0; round < 2 && rc == TTB_OK && order.size() > 1; ++round)
+    if (order.size() > 4) order.resize(4);
+    for (int round = 0; round < 3 && rc == TTB_OK && order.size() > 1; ++round)
       for (size_t i : order) timed[i].first = std::min(timed[i].first, measure(timed[i].second, 1, reps));
     float best = 1e30f;
     Prepared winner = plan->prep;

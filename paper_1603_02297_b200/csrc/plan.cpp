@@ -329,7 +329,7 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
                   b.bp = bp;
                   b.st = static_cast<int>(ns);
                   // B columns of fewer than 128 bytes make many tiny bulk copies
-                  const double small_cols = (g.mode == 2 && bp && S * ty * g.eB < 128) ? 2.0 : 0.0;
+                  const double small_cols = (g.mode == 2 && bp && run_b < 128) ? 2.0 : 0.0;
                   b.cost = 1.0 + (1.0 - ex * ey) * 12.0 + run_cost(run_a) + run_cost(run_b) +
                            std::fabs(std::log2(static_cast<double>(bytes) / 16384.0)) * 0.2 +
                            0.05 * (kx + ky) + (ns == 2 ? 0.02 : 0.0) + (1.0 - lanes) * 3.0 +

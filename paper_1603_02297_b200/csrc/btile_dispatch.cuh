@@ -1,0 +1,66 @@
+// btile_dispatch.cuh -- run-time -> template dispatch of btile_kernel for one
+// warp-role configuration (NC consumer warps, PW producer warps), shared by
+// kern_btile.cu (the default roles) and kern_btile_big.cu (large tiles).
+#pragma once
+
+#include <type_traits>
+
+#include "btile.cuh"
+#include "dispatch.cuh"
+#include "kernels.cuh"
+#include "launch.hpp"
+
+namespace ttb {
+
+// JYS: the column-walk depths instantiated (0 = linear walk)
+template <int NC, int PW, int... JYS>
+struct BtileCfg {
+  template <class F>
+  static cudaError_t with(int ka, int kb, int mode, int jy, F&& f) {
+    if (ka != kb || mode < 0 || mode > 3) return cudaErrorInvalidValue;
+    return with_types(ka, kb, [&](auto t) -> cudaError_t {
+      using T = decltype(t);
+      if constexpr (!std::is_same<typename T::SA, typename T::SB>::value) {
+        return cudaErrorInvalidValue;
+      } else {
+        auto modes = [&](auto&& g) -> cudaError_t {
+          if (mode == 3) return g(std::integral_constant<int, 3>{});
+          return with_mode(mode, g);
+        };
+        return modes([&](auto m) {
+          constexpr int M = decltype(m)::value;
+          using SA = typename T::SA;
+          cudaError_t r = cudaErrorInvalidValue;
+          ((jy == JYS ? (r = f(&btile_kernel<SA, SA, T::C, M, JYS, PW, NC>), true) : false) || ...);
+          return r;
+        });
+      }
+    });
+  }
+
+  static cudaError_t launch(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
+                            cudaStream_t s) {
+    const int jy = p.ly == 0 ? 0 : btile_rows_per_lane(p.S * p.ty, p.ly);  // ly 0: linear walk
+    return with(ka, kb, mode, jy, [&](auto fn) {
+      if (l.smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
+        if (e != cudaSuccess) return e;
+      }
+      fn<<<l.grid, l.block, l.smem, s>>>(p);
+      count_launch();
+      return cudaGetLastError();
+    });
+  }
+
+  static int occupancy(int ka, int kb, int mode, int jy, int block, int smem) {
+    int n = 0;
+    with(ka, kb, mode, jy, [&](auto fn) {
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem);
+    });
+    return n;
+  }
+};
+
+}  // namespace ttb

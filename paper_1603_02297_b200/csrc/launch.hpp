@@ -30,6 +30,9 @@ int smem_carveout();
 cudaError_t launch_btile(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                          cudaStream_t s);
 int occupancy_btile(int ka, int kb, int mode, int jy, int block, int smem);
+cudaError_t launch_btile_big(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
+                             cudaStream_t s);
+int occupancy_btile_big(int ka, int kb, int mode, int jy, int block, int smem);
 
 // data utilities (util.cu)
 struct BoxParams {

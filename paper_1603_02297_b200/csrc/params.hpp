@@ -134,6 +134,10 @@ struct SmemParams {
 // at a time, so the issue rate scales with producer warps, not lanes)
 constexpr int kBtileConsumerWarps = 4;
 constexpr int kBtileProducerWarps = 2;
+// tiles of 32 KB and more (one CTA per SM): kern_btile_big.cu
+constexpr int kBtileBigConsumerWarps = 8;
+constexpr int kBtileBigProducerWarps = 4;
+constexpr int kBtileBigTileBytes = 32 * 1024;
 
 // btile_kernel shared-memory layout of one stage (all offsets 16-byte aligned):
 //   rbase[ty]  u32: element index of tile row y's first element in the A tile

@@ -317,8 +317,11 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
                                       (g.mode == 2 && bp ? tx * (S * ty * g.eB + 32) : 0);
                 // a CTA keeps about one stage of bulk copies moving at a time, so
                 // throughput comes from 3-6 CTAs per SM with 2-3 stages each
+                // tiles of 32 KB and more run one CTA per SM with twice the
+                // warps (kern_btile_big.cu): two stages up to 200 KB
+                const bool big = !lin && bytes >= kBtileBigTileBytes;
                 for (int64_t ns : {int64_t{3}, int64_t{2}}) {
-                  if (ns * stage > 110 * 1024) continue;
+                  if (ns * stage > (big && ns == 2 ? 200 : 110) * 1024) continue;
                   Spec b;
                   b.v = kSmem;
                   b.kx = kx;
@@ -406,6 +409,16 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
                              b.tx >= 16 && static_cast<int64_t>(S) * b.ty >= 16;
       if (squareish && n < 4 && add(b)) ++n;
     }
+    n = 0;  // large tiles (512-byte runs for fp32 128 x 128): one CTA per SM;
+    // first those with >= 512-byte runs on both sides
+    for (int pass = 0; pass < 2; ++pass)
+      for (const Spec& b : bulk_specs) {
+        const int64_t bytes = static_cast<int64_t>(S) * b.tx * b.ty * std::max(g.eA, g.eB);
+        const bool long_runs = S * b.tx * g.eA >= 512 && S * b.ty * g.eB >= 512;
+        if (b.vec == 3 && b.st == 2 && bytes >= kBtileBigTileBytes && (pass || long_runs) && n < 4 &&
+            add(b))
+          ++n;
+      }
     n = 0;
     for (const Spec& b : bulk_specs)
       if (b.vec == 4 && n < 2 && add(b)) ++n;
@@ -920,7 +933,14 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
                 : static_cast<int64_t>(m.tx + m.ty) * 2 * 8 + static_cast<int64_t>(m.ty) * m.rl * g.eA;
     if (smem > 200 * 1024) return fail("smem: tile too large");
     p.l.smem = static_cast<int>(smem);
-    if (m.dense == 5) p.l.block = 32 * (kBtileConsumerWarps + kBtileProducerWarps);
+    if (m.dense == 5) {
+      // tiles of 32 KB and more: the big warp roles (column walk, 2-8 per lane)
+      const int jy = m.ly ? btile_rows_per_lane(m.S * m.ty, m.ly) : 0;
+      const int64_t tile_bytes = static_cast<int64_t>(m.S) * m.tx * m.ty * std::max(g.eA, g.eB);
+      const bool big = tile_bytes >= kBtileBigTileBytes && (jy == 2 || jy == 4 || jy == 8);
+      p.l.block = 32 * (big ? kBtileBigConsumerWarps + kBtileBigProducerWarps
+                            : kBtileConsumerWarps + kBtileProducerWarps);
+    }
     const int occ = std::min(
         occ_cap, std::max(1, m.dense == 5 ? occupancy_btile(g.ka, g.kb, p.mode, m.ly ? btile_rows_per_lane(m.S * m.ty, m.ly) : 0, p.l.block, p.l.smem) :
                              m.dense == 4 ? occupancy_vtile(g.ka, g.kb, p.mode, m.va, m.vb, m.sh, 256, p.l.smem)

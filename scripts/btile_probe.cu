@@ -84,12 +84,13 @@ int main() {
   cudaMalloc(&B, sizeof(float) * N * N);
   cudaMemset(A, 0, sizeof(float) * N * N);
   run<2, 0, 2, 4>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 4, 4>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 6, 4>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 4, 2>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 4, 8>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 8, 8>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 4, 4>(A, B, N, 64, 64, 3, 0, 0);
-  run<2, 0, 4, 4>(A, B, N, 128, 64, 2, 0, 0);
+  run<4, 0, 2, 4>(A, B, N, 128, 128, 2, 0, 0);
+  run<4, 0, 2, 8>(A, B, N, 128, 128, 2, 0, 0);
+  run<4, 0, 4, 8>(A, B, N, 128, 128, 2, 0, 0);
+  run<4, 0, 2, 4>(A, B, N, 64, 128, 2, 0, 0);
+  run<2, 0, 2, 4>(A, B, N, 128, 64, 2, 0, 0);
+  run<2, 0, 2, 4>(A, B, N, 128, 64, 3, 0, 0);
+  run<4, 0, 2, 4>(A, B, N, 96, 128, 2, 0, 0);
+  run<8, 0, 2, 8>(A, B, N, 64, 256, 2, 0, 0);
   return 0;
 }

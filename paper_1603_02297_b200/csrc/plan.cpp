@@ -403,11 +403,23 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
     };
     for (size_t i = 0; i < bulk_specs.size() && pick.size() < 4; ++i) add(bulk_specs[i]);
     int n = 0;
-    for (const Spec& b : bulk_specs) {
-      const int64_t el = static_cast<int64_t>(S) * b.tx * b.ty;
-      const bool squareish = b.vec == 3 && b.bp == 1 && b.st == 2 && el >= 2048 && el <= 8192 &&
-                             b.tx >= 16 && static_cast<int64_t>(S) * b.ty >= 16;
-      if (squareish && n < 4 && add(b)) ++n;
+    {  // the tiles closest to square runs of ~16 KB first
+      std::vector<std::pair<double, Spec>> sq;
+      for (const Spec& b : bulk_specs) {
+        const int64_t el = static_cast<int64_t>(S) * b.tx * b.ty;
+        if (!(b.vec == 3 && b.bp == 1 && b.st == 2 && el >= 2048 && el <= 8192 && b.tx >= 16 &&
+              static_cast<int64_t>(S) * b.ty >= 16))
+          continue;
+        const double ra = static_cast<double>(S * b.tx * g.eA), rb = static_cast<double>(S * b.ty * g.eB);
+        sq.emplace_back(std::fabs(std::log2(ra / rb)) + std::fabs(std::log2(static_cast<double>(el) / 4096.0)),
+                        b);
+      }
+      std::stable_sort(sq.begin(), sq.end(),
+                       [](const std::pair<double, Spec>& a, const std::pair<double, Spec>& b) {
+                         return a.first < b.first;
+                       });
+      for (const auto& q : sq)
+        if (n < 4 && add(q.second)) ++n;
     }
     n = 0;  // large tiles (512-byte runs for fp32 128 x 128): one CTA per SM;
     // first those with >= 512-byte runs on both sides

@@ -306,7 +306,16 @@ __global__ void __launch_bounds__(256) copy_rows_kernel(const CopyParams P) {
     const uint32_t seg = it - row * P.nseg;
     int64_t oa, ob;
     if (!copy_row(P, row, oa, ob)) continue;
-    const uint32_t v0 = seg * 32 * U + lane;
+    // segments start on 128-byte lines of the aligned side (P.align: 1 B, 2 A):
+    // the row's first segment is shortened by the row start's offset in its line
+    uint32_t sh = 0;
+    if (P.align) {
+      const uint64_t addr = P.align == 1 ? reinterpret_cast<uint64_t>(B + ob * C)
+                                         : reinterpret_cast<uint64_t>(A + oa * C);
+      const uint32_t vb = static_cast<uint32_t>((P.align == 1 ? sizeof(SB) : sizeof(SA)) * V * C);
+      sh = static_cast<uint32_t>((addr & 127u) / vb);
+    }
+    const uint32_t v0 = seg * 32 * U + lane - sh;  // wraps below 0: masked by v < lvec
     Vec<SA, V * C> a[U];
     Vec<SB, V * C> b[U];
 #pragma unroll

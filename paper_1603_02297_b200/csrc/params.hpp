@@ -75,6 +75,7 @@ struct CopyParams {
   uint32_t rows;          // rows including the masked rows of partial tiles
   uint32_t items;         // warp items: long rows (row, segment); short rows 32-row groups
   int long_rows;          // 1: copy_rows_kernel, 0: copy_kernel
+  int align;              // copy_rows_kernel: segments on 128-byte lines of B (1) or A (2), 0 off
 };
 
 // kRt: register micro-tile transpose between the X space (starts with A's

@@ -614,6 +614,14 @@ std::vector<Spec> candidates(const Geo& g) {
       b.tx = b.ty = 1;
       b.cost = cost + (v / w) * 0.5 - 0.1;
       out.push_back(b);
+      if (g.n[0] / w >= 128) {  // long rows: segments on 128-byte lines of B / of A
+        for (int al : {1, 2}) {
+          Spec a = b;
+          a.order = al << 1;
+          a.cost += 0.01 * al;
+          out.push_back(a);
+        }
+      }
       for (auto t : {std::pair<int, int>{1, 1}, {8, 8}, {4, 16}, {16, 4}, {32, 1}, {2, 2}}) {
         const int tx = static_cast<int>(std::min<int64_t>(t.first, pow2_ceil(nx)));
         const int ty = ky ? static_cast<int>(std::min<int64_t>(t.second, pow2_ceil(ny))) : 1;
@@ -767,15 +775,19 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     c.nyc = (c.Y.total + c.ty - 1) / c.ty;
     c.dnx = Div32::make(c.nxc);
     c.dny = Div32::make(c.nyc);
-    c.order = s.order;
+    c.order = s.order & 1;  // bit 0 tile order; order >> 1: long-row segment alignment
     const uint64_t rows = uint64_t{c.nxc} * c.nyc * c.O.total * c.tx * c.ty;  // incl. masked
     constexpr uint32_t kSeg = 32 * 8;  // vectors per warp item (copy_rows_kernel U = 8)
     c.long_rows = c.lvec >= 128 ? 1 : 0;
-    c.nseg = (c.lvec + kSeg - 1) / kSeg;
+    // long rows: segments aligned to 128-byte lines of one side (one more
+    // segment per row for the shortened first one)
+    c.align = c.long_rows ? s.order >> 1 : 0;
+    c.nseg = (c.lvec + kSeg - 1 + (c.align ? 32 : 0)) / kSeg;
     c.dseg = Div32::make(c.nseg);
     // warp items: (row, segment) for long rows, groups of 32 rows for short ones
     const uint64_t items = c.long_rows ? rows * c.nseg : (rows + 31) / 32;
-    if (rows >= kIdxLimit || items >= kIdxLimit || uint64_t{32} * c.lvec >= kIdxLimit)
+    if (rows >= kIdxLimit || items >= kIdxLimit ||
+        (!c.long_rows && uint64_t{32} * c.lvec >= kIdxLimit) || uint64_t{c.lvec} + kSeg >= kIdxLimit)
       return fail("copy: index space exceeds 2^31");
     c.rows = static_cast<uint32_t>(rows);
     c.items = static_cast<uint32_t>(items);

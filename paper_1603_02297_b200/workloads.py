@@ -102,6 +102,10 @@ PROBES: List[Workload] = [
     Workload("p_t00_a80", "s", (3, 2, 0, 4, 1), (80, 42, 11, 248, 44), 1.0, 0.0, 7000),
     Workload("p_t00_a79", "s", (3, 2, 0, 4, 1), (79, 42, 11, 245, 45), 1.0, 0.0, 7001),
     Workload("p_copy_a", "s", (0, 1), (1 << 15, 12288), 1.0, 0.0, 7002),
+    # pure streaming copy (identity, merges to rank 1) and long-row transposes
+    Workload("p_copy_1d", "d", (0, 1), (1 << 15, 6400), 1.0, 0.0, 7003),
+    Workload("p_rows_d", "d", (0, 2, 1), (1024, 400, 500), 1.0, 0.0, 7004),
+    Workload("p_rows_s", "s", (0, 2, 1), (2048, 400, 500), 1.0, 0.0, 7005),
 ]
 
 BY_NAME = {w.name: w for w in ALL + PROBES}

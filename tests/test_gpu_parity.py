@@ -385,3 +385,45 @@ def test_tune_cached_miss_then_hit(tmp_path, coracle):
     torch.cuda.synchronize()
     assert dB.cpu().numpy().tobytes() == want.tobytes()
     assert len(f.read_text().splitlines()) == 3
+
+
+def test_large_rank1_copy_every_copy_variant():
+    """An identity permutation merges to rank 1 (executor.cpp:354-355, run_copy_1d):
+    a 1.15 GB fp32 copy whose vector count exceeds the short-row kernel's 32-bit
+    group index runs on the long-row kernel, every segment alignment bit-exact."""
+    import torch
+    sizes = [1 << 14, 17500]
+    p = ttb.make_problem([1, 2], sizes, "s", "s", 1.0, 0.0)
+    n = sizes[0] * sizes[1]
+    a = ttb.TensorBuffer("s", n)
+    b = ttb.TensorBuffer("s", n)
+    ttb.fill_uniform("s", sizes, None, 77, a.data_ptr())
+    plan = ttb.GpuPlan(p, cache=False)
+    texts = plan.candidates()
+    assert any("order=2" in t for t in texts) and any("order=4" in t for t in texts)
+    for t in texts:
+        b.tensor.zero_()
+        plan.select(t)
+        plan.execute(a, b)
+        torch.cuda.synchronize()
+        assert torch.equal(a.tensor, b.tensor), t
+
+
+@pytest.mark.parametrize("ka,perm,sizes,alpha,beta", [
+    ("s", [2, 1], [1000, 1200], 1.3, 0.0),          # fp32 128x128 bulk tiles (big warp roles)
+    ("d", [2, 1], [520, 700], 0.7, 1.1),            # fp64 64x64 bulk tiles with the B ring
+    ("c", [3, 2, 1], [4, 300, 260], 1.0, 0.0),      # c4-like, complex64
+    ("s", [1, 3, 2], [49, 300, 70], 1.0, 0.5),      # c5_t10-like: shared lead S = 49
+])
+def test_medium_problems_every_variant(coracle, ka, perm, sizes, alpha, beta):
+    """Tiles of 32-64 KB only exist on problems of a few hundred per side: every
+    candidate of these (incl. the big bulk tiles) bit-exact against the oracle."""
+    rng = np.random.default_rng(sum(sizes))
+    A, B = _inputs(coracle, rng, ka, ka, perm, sizes, None, None, beta)
+    want = B.copy()
+    coracle.transpose(ka, ka, perm, sizes, None, None, alpha, A, beta, want)
+    texts = all_plans(ka, ka, perm, sizes, None, None, alpha, beta)
+    assert any("vec=3" in t or "vec=4" in t for t in texts)
+    for text in texts:
+        got = run_gpu(ka, ka, perm, sizes, None, None, alpha, A, beta, B, plan_text=text)
+        assert got.tobytes() == want.tobytes(), text

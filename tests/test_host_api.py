@@ -154,6 +154,24 @@ def test_planner_candidates_for_baseline_configs():
     assert any(s.startswith("kern=rt;mx=2;my=2") for s in plans["c4s"])
 
 
+def test_planner_offers_bulk_tiles_and_row_alignment():
+    """The bulk-copy staged tile (btile.cuh, plan text vec=3 column walk / vec=4
+    linear walk) and the long-row segment alignment (copy, order bits 1-2)."""
+    c = {w.name: ttb.debug_candidates(_problem(w)) for w in ALL}
+    # fp32 2-D: 128 x 128 tiles (512-byte runs on both sides, big warp roles)
+    assert any("tx=128;ty=128" in s and "vec=3" in s for s in c["c1"])
+    # shared stride-1 lead of 49 floats (run_case1 shape): bulk tiles of rows
+    assert any(s.startswith("kern=smem") and "vec=3" in s for s in c["c5_t10"])
+    # B lead of 2 doubles: the linear walk, and B read directly (bp=0) with beta != 0
+    assert any("vec=4" in s and "bp=0" in s for s in c["c5_t15"])
+    # long shared rows: the two segment alignments next to the plain order
+    assert any(s.startswith("kern=copy") and "order=2" in s for s in c["c5_t01"])
+    assert any(s.startswith("kern=copy") and "order=4" in s for s in c["c5_t01"])
+    # mixed kind pairs never get bulk tiles (equal kinds only)
+    p = ttb.make_problem([2, 1], [512, 640], "s", "d", 1.0, 0.0)
+    assert not any("vec=3" in s or "vec=4" in s for s in ttb.debug_candidates(p))
+
+
 def test_planner_candidates_random_problems_are_well_formed():
     rng = np.random.default_rng(7)
     for t in range(200):

@@ -278,18 +278,23 @@ bool pick_pipe(const Problem& p, HostPipe* out) {
   int64_t best_k = 0, best_w = 0;
   for (int a = 0; a < r; ++a) {
     const int64_t n = p.sizes[static_cast<size_t>(a)];
-    const int64_t k = std::min(n, kwant);
-    if (k < 2) continue;
-    const int64_t ext = (n + k - 1) / k;
     HostPipe h;
     const int q = p.perm[static_cast<size_t>(a)] - 1;
     if (!slab_side(p.sizes, p.lda, a, ea, p.footprint_a(), &h.a) ||
         !slab_side(nb, p.ldb, q, eb, p.footprint_b(), &h.b))
       continue;
-    const int64_t wa = h.a.height == 1 ? INT64_MAX : ext * h.a.stride * ea;
-    const int64_t wb = h.b.height == 1 ? INT64_MAX : ext * h.b.stride * eb;
-    const int64_t w = std::min(wa, wb);
-    if (w < min_row) continue;
+    // as many slabs as the axis allows while both sides keep rows >= min_row
+    // (fewer, wider slabs rather than no pipeline at all)
+    int64_t k = std::min(n, kwant), ext = 0, w = 0;
+    for (; k >= 2; k = k > 8 ? k * 3 / 4 : k - 1) {
+      ext = (n + k - 1) / k;
+      const int64_t wa = h.a.height == 1 ? INT64_MAX : ext * h.a.stride * ea;
+      const int64_t wb = h.b.height == 1 ? INT64_MAX : ext * h.b.stride * eb;
+      w = std::min(wa, wb);
+      if (w >= min_row) break;
+    }
+    if (k < 2) continue;
+    k = (n + ext - 1) / ext;
     if (found && (k < best_k || (k == best_k && w <= best_w))) continue;
     found = true;
     best_k = k;

@@ -140,13 +140,36 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
     const unsigned char* A = static_cast<const unsigned char*>(P.A);
     const unsigned char* Bc = static_cast<const unsigned char*>(P.B);
     uint32_t s = 0, ph = 0;
-    for (uint32_t it = blockIdx.x; it < P.items; it += g) {
+    // tiles: blockIdx.x first, then (P.ctr) the next unclaimed one from a
+    // global counter -- whole-tile work stealing, so one slow SM does not hold
+    // up the launch -- or (no counter) every g-th.  The leader lane claims and
+    // publishes the index in the stage header for the other producer warps
+    // and the consumers; the counter resets itself when the last CTA is done.
+    const bool leader = warp == NC && lane == 0;
+    uint32_t it = blockIdx.x;
+    for (uint32_t k = 0;; ++k) {
       mbar_wait(&empty[s], ph ^ 1);  // a fresh barrier passes parity 1 at once
+      unsigned char* st = stage(s);
+      volatile uint32_t* hdr = reinterpret_cast<volatile uint32_t*>(st);
+      if (k > 0) it = P.ctr ? (leader ? g + atomicAdd(P.ctr, 1u) : 0u) : it + g;
+      if (leader) *hdr = it;
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * PW) : "memory");
+      it = *hdr;
+      if (it >= P.items) {
+        mbar_arrive(&full[s]);  // consumers find the end mark in the header
+        if (leader && P.ctr) {
+          __threadfence();
+          if (atomicAdd(P.ctr + 1, 1u) == g - 1) {  // every CTA has made its last claim
+            P.ctr[0] = 0;
+            P.ctr[1] = 0;
+          }
+        }
+        break;
+      }
       const DenseTile t = dense_tile(P, it);
       int64_t aO, bO;
       decode(P.O, t.o, aO, bO);
-      unsigned char* st = stage(s);
-      uint32_t* rbase = reinterpret_cast<uint32_t*>(st);
+      uint32_t* rbase = reinterpret_cast<uint32_t*>(st + 16);
       uint32_t* boff = rbase + P.ty;
       uint32_t* cbase = boff + P.tx;
       unsigned char* ta = st + tables;
@@ -246,11 +269,13 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
   const uint32_t yi = lane & (ly - 1), xi = lane / ly;
   const uint32_t xstep = NC * lxn;
   uint32_t s = 0, ph = 0;
-  for (uint32_t it = blockIdx.x; it < P.items; it += g) {
-    const DenseTile t = dense_tile(P, it);
+  for (;;) {
     mbar_wait(&full[s], ph);
     const unsigned char* st = stage(s);
-    const uint32_t* rbase = reinterpret_cast<const uint32_t*>(st);
+    const uint32_t it = *reinterpret_cast<const volatile uint32_t*>(st);
+    if (it >= P.items) break;
+    const DenseTile t = dense_tile(P, it);
+    const uint32_t* rbase = reinterpret_cast<const uint32_t*>(st + 16);
     const uint32_t* boff = rbase + P.ty;
     const uint32_t* cbase = boff + P.tx;
     const E* ta = reinterpret_cast<const E*>(st + tables);

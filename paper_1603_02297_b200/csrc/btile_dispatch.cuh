@@ -41,12 +41,14 @@ struct BtileCfg {
   static cudaError_t launch(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                             cudaStream_t s) {
     const int jy = p.ly == 0 ? 0 : btile_rows_per_lane(p.S * p.ty, p.ly);  // ly 0: linear walk
+    SmemParams q = p;
+    q.ctr = btile_counter(s);  // null: static tile order
     return with(ka, kb, mode, jy, [&](auto fn) {
       if (l.smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
         if (e != cudaSuccess) return e;
       }
-      fn<<<l.grid, l.block, l.smem, s>>>(p);
+      fn<<<l.grid, l.block, l.smem, s>>>(q);
       count_launch();
       return cudaGetLastError();
     });

@@ -4,9 +4,32 @@
 // not through the ring), 1-16 column elements per consumer lane or the linear
 // walk (0).  Tiles of 32 KB and more run with twice the warps
 // (kern_btile_big.cu), selected by the launch's block size.
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "btile_dispatch.cuh"
 
 namespace ttb {
+
+unsigned int* btile_counter(cudaStream_t s) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, unsigned int*> counters;  // kept for the process
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = counters.find({dev, s});
+  if (it != counters.end()) return it->second;
+  void* p = nullptr;
+  if (cudaMalloc(&p, 2 * sizeof(unsigned int)) != cudaSuccess ||
+      cudaMemset(p, 0, 2 * sizeof(unsigned int)) != cudaSuccess) {
+    cudaGetLastError();
+    if (p) cudaFree(p);
+    return nullptr;
+  }
+  counters[{dev, s}] = static_cast<unsigned int*>(p);
+  return static_cast<unsigned int*>(p);
+}
 
 using BtileSmall = BtileCfg<kBtileConsumerWarps, kBtileProducerWarps, 0, 1, 2, 4, 8, 16>;
 

@@ -33,6 +33,10 @@ int occupancy_btile(int ka, int kb, int mode, int jy, int block, int smem);
 cudaError_t launch_btile_big(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                              cudaStream_t s);
 int occupancy_btile_big(int ka, int kb, int mode, int jy, int block, int smem);
+// btile_kernel's tile counter [next, done] for launches on stream s (one per
+// device and stream: launches on one stream never overlap, and the kernel
+// leaves it zeroed); null if it cannot be allocated (static tile order)
+unsigned int* btile_counter(cudaStream_t s);
 
 // data utilities (util.cu)
 struct BoxParams {

@@ -128,6 +128,7 @@ struct SmemParams {
   Div32 dplane, dgrp, dG;  // nxc*nyc, grp*nxc, grp
   Div32 dcol;              // dense == 5, linear walk: S*ty (tile column length)
   int runs;                // dense == 5: bit 0 A tile rows / bit 1 B tile columns may be contiguous
+  unsigned int* ctr;       // dense == 5: [next tile, CTAs done] for dynamic tile scheduling, or null
 };
 
 // btile_kernel warp roles: consumer warps write B; producer warps issue the
@@ -141,13 +142,14 @@ constexpr int kBtileBigProducerWarps = 4;
 constexpr int kBtileBigTileBytes = 32 * 1024;
 
 // btile_kernel shared-memory layout of one stage (all offsets 16-byte aligned):
+//   header     u32 tile index of the stage (>= items: no more tiles), 16 bytes
 //   rbase[ty]  u32: element index of tile row y's first element in the A tile
 //   boff[tx]   u32: B element offset of tile column x's first element
 //   cbase[tx]  u32: (beta != 0) element index of column x in the B tile
 //   A tile     ty rows of pa bytes
 //   B tile     (beta != 0) tx columns of pb bytes
 TTB_HD uint32_t btile_tables_bytes(uint32_t tx, uint32_t ty, bool upd) {
-  return ((ty + tx * (upd ? 2u : 1u)) * 4u + 15u) & ~15u;
+  return 16u + (((ty + tx * (upd ? 2u : 1u)) * 4u + 15u) & ~15u);  // 16: tile-index header
 }
 TTB_HD uint32_t btile_stage_bytes(uint32_t tx, uint32_t ty, uint32_t pa, uint32_t pb, bool upd) {
   return btile_tables_bytes(tx, ty, upd) + ty * pa + (upd ? tx * pb : 0u);

@@ -293,6 +293,13 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
           for (int64_t t : {1, 2, 4, 8, 16, 32, 64, 128, 256})
             if (t < N && t <= cap) v.push_back(t);
           if (N <= cap) v.push_back(N);
+          // near-equal splits of a short group (197 -> 99 + 98): no mostly
+          // empty edge tiles
+          if (N <= 4 * cap)
+            for (int64_t k = 2; k <= 8; ++k) {
+              const int64_t t = (N + k - 1) / k;
+              if (t >= 16 && t <= cap && std::find(v.begin(), v.end(), t) == v.end()) v.push_back(t);
+            }
           return v;
         };
         for (int64_t tx : bsides(NX, 1024)) {

@@ -438,9 +438,18 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
             add(b))
           ++n;
       }
-    n = 0;
+    n = 0;  // linear walks: the cheapest two, then the widest (long A rows) two
     for (const Spec& b : bulk_specs)
       if (b.vec == 4 && n < 2 && add(b)) ++n;
+    {
+      std::vector<Spec> lin;
+      for (const Spec& b : bulk_specs)
+        if (b.vec == 4) lin.push_back(b);
+      std::stable_sort(lin.begin(), lin.end(), [](const Spec& a, const Spec& b) { return a.tx > b.tx; });
+      int m = 0;
+      for (const Spec& b : lin)
+        if (m < 2 && add(b)) ++m;
+    }
     n = 0;
     for (const Spec& b : bulk_specs)
       if (b.bp == 0 && n < 2 && add(b)) ++n;

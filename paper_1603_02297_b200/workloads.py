@@ -106,6 +106,8 @@ PROBES: List[Workload] = [
     Workload("p_copy_1d", "d", (0, 1), (1 << 15, 6400), 1.0, 0.0, 7003),
     Workload("p_rows_d", "d", (0, 2, 1), (1024, 400, 500), 1.0, 0.0, 7004),
     Workload("p_rows_s", "s", (0, 2, 1), (2048, 400, 500), 1.0, 0.0, 7005),
+    Workload("p_rows_s_b", "s", (0, 2, 1), (2048, 400, 500), 1.0, 0.5, 7006, 7007),
+    Workload("p_2d_s_b", "s", (1, 0), (20480, 20480), 1.0, 0.5, 7008, 7009),
 ]
 
 BY_NAME = {w.name: w for w in ALL + PROBES}

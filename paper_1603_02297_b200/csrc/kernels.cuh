@@ -293,12 +293,19 @@ __global__ void __launch_bounds__(256) copy_kernel(const CopyParams P) {
 #ifndef TTB_ROWS_PF
 #define TTB_ROWS_PF false
 #endif
+#ifndef TTB_ROWS_MINB
+#define TTB_ROWS_MINB 2
+#endif
 template <class SA, class SB, int C, int V, int MODE>
-__global__ void __launch_bounds__(256) copy_rows_kernel(const CopyParams P) {
+__global__ void __launch_bounds__(256, TTB_ROWS_MINB) copy_rows_kernel(const CopyParams P) {
   const Update<SA, SB, MODE> up(P.sc);
   const SA* __restrict__ A = static_cast<const SA*>(P.A);
   SB* __restrict__ B = static_cast<SB*>(P.B);
-  constexpr int U = 8;
+#ifndef TTB_ROWS_U2
+#define TTB_ROWS_U2 8
+#endif
+  constexpr int U = MODE == 2 ? TTB_ROWS_U2 : 8;  // vectors per lane in flight (x2 loads with beta)
+  static_assert(8 % U == 0, "item = 8 vectors per lane");
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < P.items; it += nwarps) {
@@ -315,25 +322,29 @@ __global__ void __launch_bounds__(256) copy_rows_kernel(const CopyParams P) {
       const uint32_t vb = static_cast<uint32_t>((P.align == 1 ? sizeof(SB) : sizeof(SA)) * V * C);
       sh = static_cast<uint32_t>((addr & 127u) / vb);
     }
-    const uint32_t v0 = seg * 32 * U + lane - sh;  // wraps below 0: masked by v < lvec
-    Vec<SA, V * C> a[U];
-    Vec<SB, V * C> b[U];
+    // an item is 32 * 8 vectors (plan.cpp kSeg), moved U per lane at a time
+#pragma unroll 1
+    for (int c = 0; c < 8 / U; ++c) {
+      const uint32_t v0 = (seg * 8 + c * U) * 32 + lane - sh;  // wraps below 0: masked by v < lvec
+      Vec<SA, V * C> a[U];
+      Vec<SB, V * C> b[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t v = v0 + u * 32;
-      if (v < P.lvec) {
-        vload_a<SA, V * C, TTB_ROWS_PF>(a[u], A + (oa + static_cast<int64_t>(v) * V) * C);
-        if constexpr (MODE == 2)
-          vload_b<SB, V * C, TTB_ROWS_PF>(b[u], B + (ob + static_cast<int64_t>(v) * V) * C);
+      for (int u = 0; u < U; ++u) {
+        const uint32_t v = v0 + u * 32;
+        if (v < P.lvec) {
+          vload_a<SA, V * C, TTB_ROWS_PF>(a[u], A + (oa + static_cast<int64_t>(v) * V) * C);
+          if constexpr (MODE == 2)
+            vload_b<SB, V * C, TTB_ROWS_PF>(b[u], B + (ob + static_cast<int64_t>(v) * V) * C);
+        }
       }
-    }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t v = v0 + u * 32;
-      if (v < P.lvec) {
+      for (int u = 0; u < U; ++u) {
+        const uint32_t v = v0 + u * 32;
+        if (v < P.lvec) {
 #pragma unroll
-        for (int i = 0; i < V * C; ++i) b[u].v[i] = up(a[u].v[i], b[u].v[i]);
-        vstore(B + (ob + static_cast<int64_t>(v) * V) * C, b[u]);
+          for (int i = 0; i < V * C; ++i) b[u].v[i] = up(a[u].v[i], b[u].v[i]);
+          vstore(B + (ob + static_cast<int64_t>(v) * V) * C, b[u]);
+        }
       }
     }
   }

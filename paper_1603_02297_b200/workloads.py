@@ -108,6 +108,11 @@ PROBES: List[Workload] = [
     Workload("p_rows_s", "s", (0, 2, 1), (2048, 400, 500), 1.0, 0.0, 7005),
     Workload("p_rows_s_b", "s", (0, 2, 1), (2048, 400, 500), 1.0, 0.5, 7006, 7007),
     Workload("p_2d_s_b", "s", (1, 0), (20480, 20480), 1.0, 0.5, 7008, 7009),
+    # long-row copies: row length vs row count (c5_t19 is 600 rows of 2.6 MB)
+    Workload("p_lrow_b", "d", (0, 2, 1), (324360, 60, 10), 1.0, 0.5, 7010, 7011),
+    Workload("p_lrow_0", "d", (0, 2, 1), (324360, 60, 10), 1.0, 0.0, 7012),
+    Workload("p_mrow_b", "d", (0, 2, 1), (8192, 160, 150), 1.0, 0.5, 7013, 7014),
+    Workload("p_srow_b", "d", (0, 2, 1), (1024, 400, 475), 1.0, 0.5, 7015, 7016),
 ]
 
 BY_NAME = {w.name: w for w in ALL + PROBES}

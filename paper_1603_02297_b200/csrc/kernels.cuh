@@ -301,11 +301,10 @@ __global__ void __launch_bounds__(256, TTB_ROWS_MINB) copy_rows_kernel(const Cop
   const Update<SA, SB, MODE> up(P.sc);
   const SA* __restrict__ A = static_cast<const SA*>(P.A);
   SB* __restrict__ B = static_cast<SB*>(P.B);
-#ifndef TTB_ROWS_U2
-#define TTB_ROWS_U2 8
-#endif
-  constexpr int U = MODE == 2 ? TTB_ROWS_U2 : 8;  // vectors per lane in flight (x2 loads with beta)
-  static_assert(8 % U == 0, "item = 8 vectors per lane");
+  // an item is 4 KB of the row per warp: IT vectors per lane (rows_item_vectors),
+  // all of them in flight at once (x2 loads with beta)
+  constexpr int IT = rows_item_vectors(V * C * static_cast<int>(sizeof(SA) > sizeof(SB) ? sizeof(SA) : sizeof(SB)));
+  constexpr int U = IT;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < P.items; it += nwarps) {
@@ -322,10 +321,9 @@ __global__ void __launch_bounds__(256, TTB_ROWS_MINB) copy_rows_kernel(const Cop
       const uint32_t vb = static_cast<uint32_t>((P.align == 1 ? sizeof(SB) : sizeof(SA)) * V * C);
       sh = static_cast<uint32_t>((addr & 127u) / vb);
     }
-    // an item is 32 * 8 vectors (plan.cpp kSeg), moved U per lane at a time
 #pragma unroll 1
-    for (int c = 0; c < 8 / U; ++c) {
-      const uint32_t v0 = (seg * 8 + c * U) * 32 + lane - sh;  // wraps below 0: masked by v < lvec
+    for (int c = 0; c < IT / U; ++c) {
+      const uint32_t v0 = (seg * IT + c * U) * 32 + lane - sh;  // wraps below 0: masked by v < lvec
       Vec<SA, V * C> a[U];
       Vec<SB, V * C> b[U];
 #pragma unroll

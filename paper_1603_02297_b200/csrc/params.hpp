@@ -161,6 +161,12 @@ TTB_HD int btile_rows_per_lane(uint32_t col, uint32_t ly) {  // col = S*ty
   return n <= 1 ? 1 : n <= 2 ? 2 : n <= 4 ? 4 : n <= 8 ? 8 : 16;
 }
 
+// copy_rows_kernel: vectors per lane in one warp item (4 KB per warp for
+// vectors of up to 16 bytes; 8 for wider ones)
+TTB_HD constexpr int rows_item_vectors(int vector_bytes) {
+  return vector_bytes >= 16 ? 8 : 8 * (16 / vector_bytes);
+}
+
 // Launch shape chosen by the planner.
 struct Launch {
   int grid = 0, block = 256;

@@ -793,12 +793,13 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     c.dny = Div32::make(c.nyc);
     c.order = s.order & 1;  // bit 0 tile order; order >> 1: long-row segment alignment
     const uint64_t rows = uint64_t{c.nxc} * c.nyc * c.O.total * c.tx * c.ty;  // incl. masked
-    constexpr uint32_t kSeg = 32 * 8;  // vectors per warp item (copy_rows_kernel U = 8)
+    // vectors per warp item of copy_rows_kernel (4 KB of the row)
+    const uint32_t kSeg = 32u * static_cast<uint32_t>(rows_item_vectors(v * std::max(g.eA, g.eB)));
     c.long_rows = c.lvec >= 128 ? 1 : 0;
     // long rows: segments aligned to 128-byte lines of one side (one more
     // segment per row for the shortened first one)
     c.align = c.long_rows ? s.order >> 1 : 0;
-    c.nseg = (c.lvec + kSeg - 1 + (c.align ? 32 : 0)) / kSeg;
+    c.nseg = (c.lvec + kSeg - 1 + (c.align ? 128 : 0)) / kSeg;
     c.dseg = Div32::make(c.nseg);
     // warp items: (row, segment) for long rows, groups of 32 rows for short ones
     const uint64_t items = c.long_rows ? rows * c.nseg : (rows + 31) / 32;

@@ -302,7 +302,12 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
             }
           return v;
         };
-        for (int64_t tx : bsides(NX, 1024)) {
+        std::vector<int64_t> btx = bsides(NX, 1024);
+        if (xs.size() >= 2)  // whole multiples of X's first extent
+          for (int64_t k = 1; k <= 64 && g.n[xs[0]] * k <= std::min<int64_t>(NX, 1024); k *= 2)
+            if (std::find(btx.begin(), btx.end(), g.n[xs[0]] * k) == btx.end())
+              btx.push_back(g.n[xs[0]] * k);
+        for (int64_t tx : btx) {
           for (int64_t ty : bsides(NY, 1024)) {
             const int64_t bytes = S * tx * ty * std::max(g.eA, g.eB);
             if (bytes > 64 * 1024 || (bytes < 4 * 1024 && !(tx >= NX && ty >= NY))) continue;
@@ -728,7 +733,7 @@ std::vector<Spec> candidates(const Geo& g) {
   Spec fallback;
   bool have_fb = false;
   for (const Spec& s : out)
-    if (!have_fb && ((s.v == kSmem && s.vec != 3) || (s.v == kCopy && s.w1 == 1))) {
+    if (!have_fb && ((s.v == kSmem && s.vec < 3) || (s.v == kCopy && s.w1 == 1))) {
       fallback = s;
       fallback.vec = 0;
       have_fb = true;

@@ -211,8 +211,8 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
       // landing packed from the run's first slot; tab[i] = element index of
       // item i's first element in the region.
       auto fetch = [&](uint32_t base, uint32_t cnt, uint32_t len, int64_t off, const unsigned char* gbase,
-                       uint32_t esz, unsigned char* region, uint32_t pitch, uint32_t* tab) {
-        const uint32_t i = base + lane;
+                       uint32_t esz, unsigned char* region, uint32_t pitch, uint32_t* tab, uint32_t ti) {
+        const uint32_t i = base + lane;  // slot; the table entry is tab[ti]
         const bool valid = i < cnt;
         const int64_t prev = __shfl_up_sync(0xffffffffu, off, 1);
         const bool start = valid && (lane == 0 || prev + len != off);
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
         }
         const uint32_t s0 = valid ? 31u - __clz(smask & ((2u << lane) - 1u)) : 0u;
         const uint32_t sh0 = __shfl_sync(0xffffffffu, shift, s0);
-        if (valid) tab[i] = ((base + s0) * pitch + sh0) / esz + (lane - s0) * len;
+        if (valid) tab[ti] = ((base + s0) * pitch + sh0) / esz + (lane - s0) * len;
       };
       // one bulk copy per item (the common case: no item continues another)
       auto fetch1 = [&](uint32_t i, uint32_t len, int64_t off, const unsigned char* gbase, uint32_t esz,
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
           int64_t a = 0, b;
           const uint32_t y = base + lane;
           if (y < t.ny) decode(P.Y, t.y0 + y, a, b);
-          fetch(base, t.ny, t.nx * P.S, a + aO + t.x0 * P.S, A, EA, ta, P.pa, rbase);
+          fetch(base, t.ny, t.nx * P.S, a + aO + t.x0 * P.S, A, EA, ta, P.pa, rbase, y);
         }
       } else {
         for (uint32_t y = (warp - NC) * 32 + lane; y < t.ny; y += 32 * PW) {
@@ -261,14 +261,27 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
           fetch1(y, t.nx * P.S, a + aO + t.x0 * P.S, A, EA, ta, P.pa, rbase);
         }
       }
-      if (UPD && (P.runs & 2)) {
+      if (UPD && P.xp && t.nx == P.tx) {
+        // column-permuted walk: fetch B columns in walk order j, where
+        // consecutive columns continue each other in B
+        for (uint32_t base = (warp - NC) * 32; base < t.nx; base += 32 * PW) {
+          int64_t a, b = 0;
+          const uint32_t j = base + lane;
+          const uint32_t q2 = udiv(j, P.dxm);
+          const uint32_t x = (j - q2 * P.xm) * P.xp + q2;
+          if (j < t.nx) decode(P.X, t.x0 + x, a, b);
+          const int64_t bo = b + bO + t.y0 * P.S;
+          if (j < t.nx) boff[x] = static_cast<uint32_t>(bo);
+          fetch(base, t.nx, t.ny * P.S, bo, Bc, EB, tb, P.pb, cbase, x);
+        }
+      } else if (UPD && (P.runs & 2)) {
         for (uint32_t base = (warp - NC) * 32; base < t.nx; base += 32 * PW) {
           int64_t a, b = 0;
           const uint32_t x = base + lane;
           if (x < t.nx) decode(P.X, t.x0 + x, a, b);
           const int64_t bo = b + bO + t.y0 * P.S;
           if (x < t.nx) boff[x] = static_cast<uint32_t>(bo);
-          fetch(base, t.nx, t.ny * P.S, bo, Bc, EB, tb, P.pb, cbase);
+          fetch(base, t.nx, t.ny * P.S, bo, Bc, EB, tb, P.pb, cbase, x);
         }
       } else {
         for (uint32_t x = (warp - NC) * 32 + lane; x < t.nx; x += 32 * PW) {
@@ -313,6 +326,10 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
       // shorter than a warp (small ty, or a column run that continues into
       // the next column)
       const uint32_t Lf = P.S * P.ty, Lv = P.S * t.ny, total = Lf * t.nx;
+      // P.xp > 0 (full tiles only): a tile column is an (X0, X1) pair with X0
+      // (extent xp) covered completely and B continuing from Y into X1;
+      // walking X1 fastest keeps consecutive columns contiguous in B
+      const bool xperm = P.xp != 0 && t.nx == P.tx;
       constexpr int U = 4;
       for (uint32_t e0 = warp * 32 + lane; e0 < ((EXP & 4) ? 0u : total); e0 += U * 32 * NC) {
         EBv w[U];
@@ -321,9 +338,14 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const uint32_t e = e0 + u * 32 * NC;
-          const uint32_t x = udiv(e, P.dcol);
-          const uint32_t c = e - x * Lf;
+          const uint32_t j = udiv(e, P.dcol);  // column in walk order
+          const uint32_t c = e - j * Lf;
           v[u] = e < total && c < Lv;
+          uint32_t x = j;
+          if (xperm) {  // walk X's second axis before its first (B's order)
+            const uint32_t q2 = udiv(j, P.dxm);
+            x = (j - q2 * P.xm) * P.xp + q2;
+          }
           const uint32_t xc = v[u] ? x : 0u, cc = v[u] ? c : 0u;
           const uint32_t y = P.S == 1 ? cc : udiv(cc, P.dS);
           const E a = ta[rbase[y] + xc * P.S + (cc - y * P.S)];

@@ -129,6 +129,8 @@ struct SmemParams {
   Div32 dcol;              // dense == 5, linear walk: S*ty (tile column length)
   int runs;                // dense == 5: bit 0 A tile rows / bit 1 B tile columns may be contiguous
   unsigned int* ctr;       // dense == 5: [next tile, CTAs done] for dynamic tile scheduling, or null
+  uint32_t xp, xm;         // dense == 5, linear walk: X0 extent and tx / xp (xp 0: natural column order)
+  Div32 dxm;               // divisor xm
 };
 
 // btile_kernel warp roles: consumer warps write B; producer warps issue the

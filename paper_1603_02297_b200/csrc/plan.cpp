@@ -350,6 +350,16 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
                            0.05 * (kx + ky) + (ns == 2 ? 0.02 : 0.0) + (1.0 - lanes) * 3.0 +
                            (lin ? 0.3 : 0.0) + small_cols + (bp ? 0.0 : 0.1);
                   bulk->push_back(b);
+                  // the linear walk over (X1, X0) when B continues from Y into
+                  // X1: B runs of S*NY*tx/n0 elements, B fetched by runs
+                  if (lin && xs.size() >= 2 && tx % g.n[xs[0]] == 0 && ty >= NY &&
+                      g.sb[xs[1]] == S * NY) {
+                    Spec p2 = b;
+                    p2.xp = 1;
+                    p2.cost = b.cost - small_cols - run_cost(run_b) +
+                              run_cost(run_b * (tx / g.n[xs[0]])) - 0.05;
+                    bulk->push_back(p2);
+                  }
                 }
               }
             }
@@ -443,6 +453,9 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
             add(b))
           ++n;
       }
+    n = 0;  // column-permuted linear walks
+    for (const Spec& b : bulk_specs)
+      if (b.xp && n < 3 && add(b)) ++n;
     n = 0;  // linear walks: the cheapest two, then the widest (long A rows) two
     for (const Spec& b : bulk_specs)
       if (b.vec == 4 && n < 2 && add(b)) ++n;
@@ -542,6 +555,7 @@ std::string Spec::text() const {
                     "kern=smem;kx=%d;ky=%d;tx=%d;ty=%d;order=%d;occ=%d;st=%d;bp=%d;vec=%d", kx, ky, tx,
                     ty, order, occ, st, bp, vec);
   }
+  if (v == kSmem && xp) return std::string(buf) + ";xp=1";
   return buf;
 }
 
@@ -594,6 +608,8 @@ bool Spec::parse(const std::string& s, Spec* out) {
       p.bp = static_cast<int>(x);
     else if (k == "vec")
       p.vec = static_cast<int>(x);
+    else if (k == "xp")
+      p.xp = static_cast<int>(x);
     else
       return false;
   }
@@ -736,6 +752,7 @@ std::vector<Spec> candidates(const Geo& g) {
     if (!have_fb && ((s.v == kSmem && s.vec < 3) || (s.v == kCopy && s.w1 == 1))) {
       fallback = s;
       fallback.vec = 0;
+      fallback.xp = 0;
       have_fb = true;
     }
   // cap the list but keep every family represented: the best few copy and
@@ -923,6 +940,18 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
       // Y's first axis follows X in A; likewise B columns
       m.runs = ((m.tx >= m.X.total && g.sa[ys[0]] == static_cast<int64_t>(m.S) * m.X.total) ? 1 : 0) |
                ((m.ty >= m.Y.total && g.sb[xs[0]] == static_cast<int64_t>(m.S) * m.Y.total) ? 2 : 0);
+      m.xp = m.xm = 0;
+      m.dxm = Div32::make(1);
+      if (s.xp) {
+        // X = (X0, X1, ...) with tiles of whole X0 ranges, the tile spanning
+        // Y, and B continuing from Y into X1 (the linear walk only)
+        if (!(lin && xs.size() >= 2 && m.tx % g.n[xs[0]] == 0 && m.ty >= m.Y.total &&
+              g.sb[xs[1]] == static_cast<int64_t>(m.S) * m.Y.total))
+          return fail("smem: column permutation not applicable");
+        m.xp = static_cast<uint32_t>(g.n[xs[0]]);
+        m.xm = m.tx / m.xp;
+        m.dxm = Div32::make(m.xm);
+      }
       // a row's 16-byte superset spans at most tx*e + 16 - e bytes; an odd
       // number of 16-byte units keeps 8 consecutive rows on distinct banks
       auto pitch = [](uint32_t n, int e) {

@@ -43,6 +43,7 @@ struct Spec {
   int st = 2;          // smem: cp.async pipeline stages (dense tiles: 2 or 3)
   int bp = 1;          // smem, beta != 0: B through the cp.async ring (1) or direct (0)
   int vec = 1;         // smem: vector tile kernel where the strides allow it (0: element-wise)
+  int xp = 0;          // smem, linear-walk bulk tile: walk X's second axis first (in the text only when 1)
   double cost = 0;     // heuristic rank (lower first)
 
   std::string text() const;

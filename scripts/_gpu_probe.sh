@@ -1,1 +1,2 @@
-for pl in "kern=smem;kx=2;ky=1;tx=256;ty=2;order=0;occ=0;st=3;bp=1;vec=4" "kern=smem;kx=2;ky=1;tx=512;ty=2;order=0;occ=0;st=3;bp=1;vec=4" "kern=smem;kx=2;ky=1;tx=1024;ty=2;order=0;occ=0;st=2;bp=1;vec=4" "kern=smem;kx=2;ky=1;tx=512;ty=2;order=0;occ=0;st=3;bp=0;vec=4" "kern=smem;kx=2;ky=1;tx=1024;ty=2;order=0;occ=0;st=2;bp=0;vec=4" "kern=smem;kx=1;ky=1;tx=54;ty=2;order=0;occ=0;st=3;bp=1;vec=4" "kern=smem;kx=2;ky=1;tx=256;ty=2;order=0;occ=0;st=3;bp=0;vec=4"; do timeout 300 python scripts/run_case.py c5_t15 --iters 5 --check --plan "$pl" >> gpurun_out/cands_t15.log 2>&1; done
+timeout 600 python scripts/dbg_plans.py xp= > gpurun_out/dbg_plans.log 2>&1
+for c in c5_t18 c5_t08; do timeout 300 python scripts/run_case.py $c --iters 5 --check > gpurun_out/cands_$c.log 2>&1; done

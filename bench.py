@@ -205,7 +205,7 @@ class Row:
 
     def autotune(self):
         for plan, pa, pb, q, _, _ in self.plans:
-            plan.autotune(pa, pb, warmups=2, reps=4)
+            plan.autotune(pa, pb, warmups=2, reps=6)
 
     def refill_b(self):
         """beta != 0: restore B after tuning so the verified run is one application."""
@@ -382,7 +382,7 @@ def bench_configs(torch, ttb, peak, d2d):
         ttb.fill_sentinel(w.kind, na, a.data_ptr())
         ttb.fill_uniform(w.kind, list(w.sizes), w.lda and list(w.lda), w.seed_a, a.data_ptr())
         plan = ttb.GpuPlan(p)
-        plan.autotune(a, b, warmups=2, reps=4)
+        plan.autotune(a, b, warmups=2, reps=6)
         if w.beta != 0.0:
             ttb.fill_uniform(w.kind, w.sizes_b, w.ldb and list(w.ldb), w.seed_b, b.data_ptr())
         plan.execute(a, b)

@@ -414,6 +414,7 @@ def test_large_rank1_copy_every_copy_variant():
     ("d", [2, 1], [520, 700], 0.7, 1.1),            # fp64 64x64 bulk tiles with the B ring
     ("c", [3, 2, 1], [4, 300, 260], 1.0, 0.0),      # c4-like, complex64
     ("s", [1, 3, 2], [49, 300, 70], 1.0, 0.5),      # c5_t10-like: shared lead S = 49
+    ("s", [5, 2, 4, 1, 3], [10, 64, 6, 36, 5], 1.0, 0.5),  # c5_t18-like: column-permuted walk (xp)
 ])
 def test_medium_problems_every_variant(coracle, ka, perm, sizes, alpha, beta):
     """Tiles of 32-64 KB only exist on problems of a few hundred per side: every

@@ -137,7 +137,7 @@ struct SmemParams {
 // bulk copies (issued per warp through the uniform datapath, one lane's copy
 // at a time, so the issue rate scales with producer warps, not lanes)
 constexpr int kBtileConsumerWarps = 4;
-constexpr int kBtileProducerWarps = 2;
+constexpr int kBtileProducerWarps = 4;
 // tiles of 32 KB and more (one CTA per SM): kern_btile_big.cu
 constexpr int kBtileBigConsumerWarps = 8;
 constexpr int kBtileBigProducerWarps = 4;

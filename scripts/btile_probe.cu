@@ -20,13 +20,13 @@ static Space space1(uint32_t n, int64_t sa, int64_t sb) {
   return s;
 }
 
-template <int JY, int EXP, int PW = 4, int NC = 8>
+template <int JY, int EXP, int PW = 4, int NC = 8, int MODE = 0>
 float run(const float* A, float* B, uint32_t N, uint32_t tx, uint32_t ty, uint32_t ns, int ctas,
           int order = 0) {
   SmemParams P{};
   P.A = A;
   P.B = B;
-  P.sc = Scale{1.0, 0.0};
+  P.sc = Scale{1.0, MODE >= 2 ? 0.5 : 0.0};
   P.X = space1(N, 1, N);  // A axis 0: stride 1 in A, stride N in B
   P.Y = space1(N, N, 1);
   P.O = Space{};
@@ -49,10 +49,10 @@ float run(const float* A, float* B, uint32_t N, uint32_t tx, uint32_t ty, uint32
   P.ly = 32;
   P.pa = ((tx * 4 + 12 + 15) & ~15u);
   if ((P.pa / 16) % 2 == 0) P.pa += 16;
-  P.pb = 16;
+  P.pb = ((ty * 4 + 12 + 15) & ~15u);
   P.ns = ns;
-  const int smem = ns * btile_stage_bytes(tx, ty, P.pa, P.pb, false);
-  auto fn = &btile_kernel<float, float, 1, 0, JY, PW, NC, EXP>;
+  const int smem = ns * btile_stage_bytes(tx, ty, P.pa, P.pb, MODE == 2);
+  auto fn = &btile_kernel<float, float, 1, MODE, JY, PW, NC, EXP>;
   const int block = 32 * (NC + PW);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int occ = 0;
@@ -71,26 +71,27 @@ float run(const float* A, float* B, uint32_t N, uint32_t tx, uint32_t ty, uint32
     cudaEventElapsedTime(&ms, e0, e1);
     if (it && ms < best) best = ms;
   }
-  const double gbs = 2.0 * 4.0 * N * N / (best * 1e6);
-  printf("order=%d N=%u nc=%d pw=%d tile %ux%u ns=%u occ=%d grid=%d exp=%d: %.1f us %.1f GB/s  (%s)\n", order, N, NC, PW, tx, ty, ns,
+  const double gbs = (MODE >= 2 ? 3.0 : 2.0) * 4.0 * N * N / (best * 1e6);
+  printf("mode=%d order=%d N=%u nc=%d pw=%d tile %ux%u ns=%u occ=%d grid=%d exp=%d: %.1f us %.1f GB/s  (%s)\n", MODE, order, N, NC, PW, tx, ty, ns,
          occ, grid, EXP, best * 1e3, gbs, cudaGetErrorString(cudaGetLastError()));
   return best;
 }
 
 int main() {
-  const uint32_t N = 7264 * 2;
+  const uint32_t N = 14527;  // odd: every tile row / column misaligned
   float *A, *B;
   cudaMalloc(&A, sizeof(float) * N * N);
   cudaMalloc(&B, sizeof(float) * N * N);
   cudaMemset(A, 0, sizeof(float) * N * N);
-  run<2, 0, 2, 4>(A, B, N, 64, 64, 2, 0, 0);
-  run<4, 0, 2, 4>(A, B, N, 128, 128, 2, 0, 0);
-  run<4, 0, 2, 8>(A, B, N, 128, 128, 2, 0, 0);
-  run<4, 0, 4, 8>(A, B, N, 128, 128, 2, 0, 0);
-  run<4, 0, 2, 4>(A, B, N, 64, 128, 2, 0, 0);
-  run<2, 0, 2, 4>(A, B, N, 128, 64, 2, 0, 0);
-  run<2, 0, 2, 4>(A, B, N, 128, 64, 3, 0, 0);
-  run<4, 0, 2, 4>(A, B, N, 96, 128, 2, 0, 0);
-  run<8, 0, 2, 8>(A, B, N, 64, 256, 2, 0, 0);
+  run<2, 0, 2, 4, 0>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 2, 4, 2>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 4, 4, 2>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 2, 8, 2>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 4, 8, 2>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 2, 4, 3>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 2, 4, 2>(A, B, N, 48, 64, 2, 0, 0);
+  run<2, 0, 4, 4, 2>(A, B, N, 48, 64, 2, 0, 0);
+  run<2, 0, 2, 4, 2>(A, B, N, 64, 64, 3, 0, 0);
+  run<4, 0, 4, 8, 0>(A, B, N, 128, 128, 2, 0, 0);
   return 0;
 }

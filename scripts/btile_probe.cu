@@ -83,15 +83,15 @@ int main() {
   cudaMalloc(&A, sizeof(float) * N * N);
   cudaMalloc(&B, sizeof(float) * N * N);
   cudaMemset(A, 0, sizeof(float) * N * N);
-  run<2, 0, 2, 4, 0>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 2, 4, 2>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 4, 4, 2>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 2, 8, 2>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 4, 8, 2>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 2, 4, 3>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 2, 4, 2>(A, B, N, 48, 64, 2, 0, 0);
-  run<2, 0, 4, 4, 2>(A, B, N, 48, 64, 2, 0, 0);
-  run<2, 0, 2, 4, 2>(A, B, N, 64, 64, 3, 0, 0);
   run<4, 0, 4, 8, 0>(A, B, N, 128, 128, 2, 0, 0);
+  run<4, 0, 8, 8, 0>(A, B, N, 128, 128, 2, 0, 0);
+  run<4, 0, 6, 8, 0>(A, B, N, 128, 128, 2, 0, 0);
+  run<2, 0, 4, 8, 2>(A, B, N, 128, 64, 2, 0, 0);
+  run<2, 0, 8, 8, 2>(A, B, N, 128, 64, 2, 0, 0);
+  run<4, 0, 4, 8, 2>(A, B, N, 64, 128, 2, 0, 0);
+  run<4, 0, 8, 8, 2>(A, B, N, 64, 128, 2, 0, 0);
+  run<2, 0, 4, 4, 2>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 6, 4, 2>(A, B, N, 64, 64, 2, 0, 0);
+  run<2, 0, 4, 4, 0>(A, B, N, 64, 64, 2, 0, 1);
   return 0;
 }

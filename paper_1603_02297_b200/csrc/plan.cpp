@@ -472,6 +472,17 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
     for (const Spec& b : bulk_specs)
       if (b.bp == 0 && n < 2 && add(b)) ++n;
     for (const Spec& b : pick) out->push_back(b);
+    // and every pick with Y chunks fastest: tiles that share a B column's
+    // ragged 32-byte sectors are then in flight together, so L2 merges the
+    // partial writes instead of evicting them half-written
+    if (g.mode != 2)
+      for (const Spec& b : pick)
+        if (b.order == 0) {
+          Spec o = b;
+          o.order = 1;
+          o.cost += 0.01;
+          out->push_back(o);
+        }
   }
   for (size_t i = 0; i < cand.size() && i < 8; ++i) {
     out->push_back(cand[i]);
@@ -757,12 +768,12 @@ std::vector<Spec> candidates(const Geo& g) {
     }
   // cap the list but keep every family represented: the best few copy and
   // register-transpose candidates survive even when staged tiles rank higher
-  if (out.size() > 40) {
-    std::vector<Spec> kept(out.begin(), out.begin() + 40);
+  if (out.size() > 56) {
+    std::vector<Spec> kept(out.begin(), out.begin() + 56);
     for (Variant v : {kCopy, kRt}) {
       int have = 0;
       for (const Spec& k : kept) have += k.v == v;
-      for (size_t i = 40; i < out.size() && have < 4; ++i)
+      for (size_t i = 56; i < out.size() && have < 4; ++i)
         if (out[i].v == v) {
           kept.push_back(out[i]);
           ++have;

@@ -6,15 +6,18 @@
 // global -> shared side is one cp.async.bulk per tile row instead of one
 // LDGSTS per element or 16-byte chunk, and the kernel is warp specialised:
 //
-//   warps NC..NC+PW-1   (producers) for every tile of this CTA: wait until the ring stage
+//   warps NC..NC+PW-1   (producers) claim the next tile (a global counter:
+//                       whole-tile work stealing), wait until the ring stage
 //                       is free, decode the tile's row / column offsets (one
-//                       lane per row / column), issue a bulk copy of each A
-//                       tile row -- and with beta != 0 of each B tile column --
-//                       into the stage, write the offset tables, arrive on the
-//                       stage's `full` mbarrier with the byte count.
+//                       lane per row / column), issue a bulk copy per A tile
+//                       row -- and with beta != 0 per B tile column; rows or
+//                       columns that continue each other go as one copy --
+//                       write the offset tables and the tile index into the
+//                       stage, and arrive on its `full` mbarrier with the bytes.
 //   warps 0..NC-1       wait on `full`, write the tile to B with lanes along
-//                       B's stride-1 index (coalesced stores, alpha/beta
-//                       epilogue fused), release the stage on `empty`.
+//                       B's stride-1 run (column walk) or along the whole tile
+//                       in B order (linear walk), alpha/beta fused (MODE 3: B
+//                       read directly, not through the ring), release `empty`.
 //
 // Bulk copies need 16-byte aligned addresses and sizes: a row that starts or
 // ends inside a 16-byte block is fetched as the aligned superset of blocks that
@@ -24,10 +27,10 @@
 // element bytes; the consumer reads element x of row y at y*pitch + d(y) + x.
 // Bytes of the superset outside the logical row are never used.
 //
-// The ring has NS stages (NS - 1 tiles of loads in flight while a tile is
-// written out), so the bytes in flight per SM are set by shared memory, not by
-// registers or by how many threads issue loads -- the element-wise kernels
-// (dense_kernel, tile_kernel) stall on exactly that with misaligned f32 rows.
+// Measured on B200: copies are issued one lane at a time through
+// the uniform datapath and a CTA keeps about one stage of them moving, so the
+// throughput comes from producer warps (4) and CTAs per SM (3-6, 2-3 stages
+// each), or from large tiles (kern_btile_big.cu) -- not from deeper rings.
 #pragma once
 
 #include "kernels.cuh"

@@ -453,6 +453,20 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
             add(b))
           ++n;
       }
+    {  // the square-ish column walks again with 8 / 16 lanes per column
+      // (8 rows x 4 columns per warp: fewer shared-memory bank conflicts)
+      std::vector<Spec> more;
+      for (const Spec& b : pick)
+        if (b.vec == 3 && b.st == 2 && static_cast<int64_t>(S) * b.tx * b.ty * std::max(g.eA, g.eB) < kBtileBigTileBytes)
+          for (int l : {8, 16})
+            if (S * b.ty >= 2 * l && S * b.ty <= 16 * l && more.size() < 8) {
+              Spec o = b;
+              o.ly = l;
+              o.cost += 0.01;
+              more.push_back(o);
+            }
+      for (const Spec& o : more) add(o);
+    }
     n = 0;  // column-permuted linear walks
     for (const Spec& b : bulk_specs)
       if (b.xp && n < 3 && add(b)) ++n;
@@ -566,8 +580,10 @@ std::string Spec::text() const {
                     "kern=smem;kx=%d;ky=%d;tx=%d;ty=%d;order=%d;occ=%d;st=%d;bp=%d;vec=%d", kx, ky, tx,
                     ty, order, occ, st, bp, vec);
   }
-  if (v == kSmem && xp) return std::string(buf) + ";xp=1";
-  return buf;
+  std::string t = buf;
+  if (v == kSmem && xp) t += ";xp=1";
+  if (v == kSmem && ly) t += ";ly=" + std::to_string(ly);
+  return t;
 }
 
 bool Spec::parse(const std::string& s, Spec* out) {
@@ -621,6 +637,8 @@ bool Spec::parse(const std::string& s, Spec* out) {
       p.vec = static_cast<int>(x);
     else if (k == "xp")
       p.xp = static_cast<int>(x);
+    else if (k == "ly")
+      p.ly = static_cast<int>(x);
     else
       return false;
   }
@@ -764,6 +782,7 @@ std::vector<Spec> candidates(const Geo& g) {
       fallback = s;
       fallback.vec = 0;
       fallback.xp = 0;
+      fallback.ly = 0;
       have_fb = true;
     }
   // cap the list but keep every family represented: the best few copy and
@@ -945,6 +964,11 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
       m.ept = 0;
       m.ly = 1;
       while (m.ly < 32 && m.ly < m.S * m.ty) m.ly *= 2;
+      if (s.ly) {  // fewer lanes per column, more columns per warp step
+        if (lin || (s.ly != 8 && s.ly != 16) || m.S * m.ty > 16u * static_cast<uint32_t>(s.ly))
+          return fail("smem: lanes per column not applicable");
+        m.ly = std::min<uint32_t>(m.ly, static_cast<uint32_t>(s.ly));
+      }
       if (lin) m.ly = 0;
       m.dcol = Div32::make(m.S * m.ty);
       // consecutive tile rows are contiguous in A when the tile spans X and

@@ -44,6 +44,7 @@ struct Spec {
   int bp = 1;          // smem, beta != 0: B through the cp.async ring (1) or direct (0)
   int vec = 1;         // smem: vector tile kernel where the strides allow it (0: element-wise)
   int xp = 0;          // smem, linear-walk bulk tile: walk X's second axis first (in the text only when 1)
+  int ly = 0;          // smem, column-walk bulk tile: lanes along a column (0: up to 32; text only when set)
   double cost = 0;     // heuristic rank (lower first)
 
   std::string text() const;

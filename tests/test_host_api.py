@@ -167,6 +167,8 @@ def test_planner_offers_bulk_tiles_and_row_alignment():
     # long shared rows: the two segment alignments next to the plain order
     assert any(s.startswith("kern=copy") and "order=2" in s for s in c["c5_t01"])
     assert any(s.startswith("kern=copy") and "order=4" in s for s in c["c5_t01"])
+    # column walks with 8 / 16 lanes per column (8 x 4 rows x columns per warp)
+    assert any("vec=3" in s and s.endswith("ly=8") for s in c["c5_t22"])
     # B continuing from Y into X's second axis: the column-permuted linear walk
     assert any("vec=4" in s and s.endswith("xp=1") for s in c["c5_t18"])
     # mixed kind pairs never get bulk tiles (equal kinds only)

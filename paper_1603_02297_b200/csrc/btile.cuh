@@ -98,26 +98,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// the same with an L2 eviction-priority policy (createpolicy): A is read once
-__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                              uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-
-#ifndef TTB_BTILE_EVICT_FIRST
-#define TTB_BTILE_EVICT_FIRST 0  // measured: no gain, -5% on 128x128 tiles
-#endif
-
 // (stage layout: btile_stage_bytes, params.hpp)
 
 // P.ns stages, P.pa / P.pb row / column pitches (bytes), P.ly lanes along a
@@ -169,7 +149,6 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
     // publishes the index in the stage header for the other producer warps
     // and the consumers; the counter resets itself when the last CTA is done.
     const bool leader = warp == NC && lane == 0;
-    const uint64_t pol = l2_evict_first_policy();
     uint32_t it = blockIdx.x;
     for (uint32_t k = 0;; ++k) {
       mbar_wait(&empty[s], ph ^ 1);  // a fresh barrier passes parity 1 at once
@@ -199,12 +178,8 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
       unsigned char* ta = st + tables;
       unsigned char* tb = ta + P.ty * P.pa;
       uint32_t bytes = 0;
-      // A is read exactly once: its bulk copies carry an L2 evict-first policy
-      auto copy = [&](unsigned char* dst, uint64_t src, uint32_t n, bool is_a) {
-        if (TTB_BTILE_EVICT_FIRST && is_a)
-          bulk_g2s_hint(dst, reinterpret_cast<const void*>(src), n, &full[s], pol);
-        else
-          bulk_g2s(dst, reinterpret_cast<const void*>(src), n, &full[s]);
+      auto copy = [&](unsigned char* dst, uint64_t src, uint32_t n) {
+        bulk_g2s(dst, reinterpret_cast<const void*>(src), n, &full[s]);
       };
       // P.runs bit 0 / 1: A rows / B columns may continue each other (the
       // planner's static test); then items are handled 32 at a time per warp:
@@ -230,7 +205,7 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
           const uint64_t hi = (ga + static_cast<uint64_t>(end - lane) * len * esz + 15) & ~uint64_t{15};
           shift = static_cast<uint32_t>(ga - lo);
           if constexpr (!(EXP & 2)) {
-            copy(region + i * pitch, lo, static_cast<uint32_t>(hi - lo), gbase == A);
+            copy(region + i * pitch, lo, static_cast<uint32_t>(hi - lo));
             bytes += static_cast<uint32_t>(hi - lo);
           }
         }
@@ -245,7 +220,7 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
         const uint64_t lo = ga & ~uint64_t{15};
         const uint64_t hi = (ga + static_cast<uint64_t>(len) * esz + 15) & ~uint64_t{15};
         if constexpr (!(EXP & 2)) {
-          copy(region + i * pitch, lo, static_cast<uint32_t>(hi - lo), gbase == A);
+          copy(region + i * pitch, lo, static_cast<uint32_t>(hi - lo));
           bytes += static_cast<uint32_t>(hi - lo);
         }
         tab[i] = (i * pitch + static_cast<uint32_t>(ga - lo)) / esz;

@@ -86,17 +86,10 @@ struct alignas((sizeof(T) * N) >= 16 ? 16 : (sizeof(T) * N)) Vec {
   T v[N];
 };
 
-// streaming read-only load of one <=16-byte chunk (A is never written);
-// PF: ask L2 to fetch the whole 256-byte block (long contiguous rows only)
-template <int BYTES, bool PF = false>
+// streaming read-only load of one <=16-byte chunk (A is never written)
+template <int BYTES>
 __device__ __forceinline__ void ld_nc(const void* p, void* out) {
-  if constexpr (BYTES == 16 && PF) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    *reinterpret_cast<uint4*>(out) = r;
-  } else if constexpr (BYTES == 16) {
+  if constexpr (BYTES == 16) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
@@ -117,15 +110,9 @@ __device__ __forceinline__ void ld_nc(const void* p, void* out) {
 }
 
 // load of B for the beta != 0 update (B is read once, then overwritten)
-template <int BYTES, bool PF = false>
+template <int BYTES>
 __device__ __forceinline__ void ld_b(const void* p, void* out) {
-  if constexpr (BYTES == 16 && PF) {
-    uint4 r;
-    asm volatile("ld.global.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    *reinterpret_cast<uint4*>(out) = r;
-  } else if constexpr (BYTES == 16) {
+  if constexpr (BYTES == 16) {
     uint4 r;
     asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
@@ -161,22 +148,22 @@ __device__ __forceinline__ void st_g(void* p, const void* in) {
 }
 
 // whole-vector helpers: vectors of up to 32 bytes move as <=16-byte chunks
-template <class T, int N, bool PF = false>
+template <class T, int N>
 __device__ __forceinline__ void vload_a(Vec<T, N>& v, const T* p) {
   constexpr int BYTES = sizeof(T) * N;
   constexpr int CH = BYTES > 16 ? 16 : BYTES;
 #pragma unroll
   for (int c = 0; c < BYTES / CH; ++c)
-    ld_nc<CH, PF>(reinterpret_cast<const char*>(p) + c * CH, reinterpret_cast<char*>(v.v) + c * CH);
+    ld_nc<CH>(reinterpret_cast<const char*>(p) + c * CH, reinterpret_cast<char*>(v.v) + c * CH);
 }
 
-template <class T, int N, bool PF = false>
+template <class T, int N>
 __device__ __forceinline__ void vload_b(Vec<T, N>& v, const T* p) {
   constexpr int BYTES = sizeof(T) * N;
   constexpr int CH = BYTES > 16 ? 16 : BYTES;
 #pragma unroll
   for (int c = 0; c < BYTES / CH; ++c)
-    ld_b<CH, PF>(reinterpret_cast<const char*>(p) + c * CH, reinterpret_cast<char*>(v.v) + c * CH);
+    ld_b<CH>(reinterpret_cast<const char*>(p) + c * CH, reinterpret_cast<char*>(v.v) + c * CH);
 }
 
 template <class T, int N>
@@ -287,12 +274,7 @@ __global__ void __launch_bounds__(256) copy_kernel(const CopyParams P) {
 }
 
 // Shared stride-1 index, long rows: a warp streams one segment of 32*U
-// vectors of a row per item (row offsets decoded once per item).  The loads
-// carry the L2 256-byte prefetch hint (a warp's 32 lanes read contiguous
-// 16-byte vectors of the same row).
-#ifndef TTB_ROWS_PF
-#define TTB_ROWS_PF false
-#endif
+// vectors of a row per item (row offsets decoded once per item).
 #ifndef TTB_ROWS_MINB
 #define TTB_ROWS_MINB 2
 #endif
@@ -330,9 +312,9 @@ __global__ void __launch_bounds__(256, TTB_ROWS_MINB) copy_rows_kernel(const Cop
       for (int u = 0; u < U; ++u) {
         const uint32_t v = v0 + u * 32;
         if (v < P.lvec) {
-          vload_a<SA, V * C, TTB_ROWS_PF>(a[u], A + (oa + static_cast<int64_t>(v) * V) * C);
+          vload_a(a[u], A + (oa + static_cast<int64_t>(v) * V) * C);
           if constexpr (MODE == 2)
-            vload_b<SB, V * C, TTB_ROWS_PF>(b[u], B + (ob + static_cast<int64_t>(v) * V) * C);
+            vload_b(b[u], B + (ob + static_cast<int64_t>(v) * V) * C);
         }
       }
 #pragma unroll

@@ -1,2 +1,2 @@
-timeout 600 python scripts/dbg_plans.py vec=3 > gpurun_out/dbg_plans.log 2>&1
-timeout 900 python bench.py --no-e2e --no-cpu > gpurun_out/bench_full.log 2>&1; echo rc=$? >> gpurun_out/bench_full.log
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/pytest_gpu.log
+for c in c5_t00 c5_t19 c5_t22; do timeout 300 python scripts/run_case.py $c --iters 5 --check --top 3 > gpurun_out/cands_$c.log 2>&1; done

@@ -22,7 +22,7 @@ static Space space1(uint32_t n, int64_t sa, int64_t sb) {
 
 template <int JY, int EXP, int PW = 4, int NC = 8, int MODE = 0>
 float run(const float* A, float* B, uint32_t N, uint32_t tx, uint32_t ty, uint32_t ns, int ctas,
-          int order = 0) {
+          int order = 0, uint32_t ly = 32) {
   SmemParams P{};
   P.A = A;
   P.B = B;
@@ -46,7 +46,7 @@ float run(const float* A, float* B, uint32_t N, uint32_t tx, uint32_t ty, uint32
   P.dG = Div32::make(P.grp);
   P.items = P.nxc * P.nyc;
   P.dense = 5;
-  P.ly = 32;
+  P.ly = ly;
   P.pa = ((tx * 4 + 12 + 15) & ~15u);
   if ((P.pa / 16) % 2 == 0) P.pa += 16;
   P.pb = ((ty * 4 + 12 + 15) & ~15u);
@@ -72,7 +72,7 @@ float run(const float* A, float* B, uint32_t N, uint32_t tx, uint32_t ty, uint32
     if (it && ms < best) best = ms;
   }
   const double gbs = (MODE >= 2 ? 3.0 : 2.0) * 4.0 * N * N / (best * 1e6);
-  printf("mode=%d order=%d N=%u nc=%d pw=%d tile %ux%u ns=%u occ=%d grid=%d exp=%d: %.1f us %.1f GB/s  (%s)\n", MODE, order, N, NC, PW, tx, ty, ns,
+  printf("ly=%u mode=%d order=%d N=%u nc=%d pw=%d tile %ux%u ns=%u occ=%d grid=%d exp=%d: %.1f us %.1f GB/s  (%s)\n", ly, MODE, order, N, NC, PW, tx, ty, ns,
          occ, grid, EXP, best * 1e3, gbs, cudaGetErrorString(cudaGetLastError()));
   return best;
 }
@@ -83,15 +83,14 @@ int main() {
   cudaMalloc(&A, sizeof(float) * N * N);
   cudaMalloc(&B, sizeof(float) * N * N);
   cudaMemset(A, 0, sizeof(float) * N * N);
-  run<4, 0, 4, 8, 0>(A, B, N, 128, 128, 2, 0, 0);
-  run<4, 0, 8, 8, 0>(A, B, N, 128, 128, 2, 0, 0);
-  run<4, 0, 6, 8, 0>(A, B, N, 128, 128, 2, 0, 0);
-  run<2, 0, 4, 8, 2>(A, B, N, 128, 64, 2, 0, 0);
-  run<2, 0, 8, 8, 2>(A, B, N, 128, 64, 2, 0, 0);
-  run<4, 0, 4, 8, 2>(A, B, N, 64, 128, 2, 0, 0);
-  run<4, 0, 8, 8, 2>(A, B, N, 64, 128, 2, 0, 0);
-  run<2, 0, 4, 4, 2>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 6, 4, 2>(A, B, N, 64, 64, 2, 0, 0);
-  run<2, 0, 4, 4, 0>(A, B, N, 64, 64, 2, 0, 1);
+  run<2, 0, 4, 4, 2>(A, B, N, 64, 64, 2, 0, 0, 32);
+  run<8, 0, 4, 4, 2>(A, B, N, 64, 64, 2, 0, 0, 8);
+  run<4, 0, 4, 4, 2>(A, B, N, 64, 64, 2, 0, 0, 16);
+  run<2, 0, 4, 4, 0>(A, B, N, 64, 64, 2, 0, 1, 32);
+  run<8, 0, 4, 4, 0>(A, B, N, 64, 64, 2, 0, 1, 8);
+  run<4, 0, 4, 4, 0>(A, B, N, 64, 64, 2, 0, 1, 16);
+  run<4, 0, 4, 8, 0>(A, B, N, 128, 128, 2, 0, 0, 32);
+  run<16, 0, 4, 8, 0>(A, B, N, 128, 128, 2, 0, 0, 8);
+  run<8, 0, 4, 8, 0>(A, B, N, 128, 128, 2, 0, 0, 16);
   return 0;
 }

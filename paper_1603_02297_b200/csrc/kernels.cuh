@@ -275,11 +275,10 @@ __global__ void __launch_bounds__(256) copy_kernel(const CopyParams P) {
 
 // Shared stride-1 index, long rows: a warp streams one segment of 32*U
 // vectors of a row per item (row offsets decoded once per item).
-#ifndef TTB_ROWS_MINB
-#define TTB_ROWS_MINB 2
-#endif
+// Resident CTAs per SM: 4 without B loads (more warps hide the load latency),
+// 2 with them (twice the registers in flight; 4 would spill).
 template <class SA, class SB, int C, int V, int MODE>
-__global__ void __launch_bounds__(256, TTB_ROWS_MINB) copy_rows_kernel(const CopyParams P) {
+__global__ void __launch_bounds__(256, MODE == 2 ? 2 : 4) copy_rows_kernel(const CopyParams P) {
   const Update<SA, SB, MODE> up(P.sc);
   const SA* __restrict__ A = static_cast<const SA*>(P.A);
   SB* __restrict__ B = static_cast<SB*>(P.B);

@@ -91,19 +91,51 @@ def config_block(n):
 # ------------------------------------------------------------------ clocks --
 
 class ClockSampler:
+    """SM clocks and throttle reasons during the timed region: NVML polled every
+    10 ms from a thread (pynvml), else `nvidia-smi -lms 200`.  Both write the
+    same CSV rows (index, sm, max sm, power, reasons..., hw_slowdown,
+    hw_thermal_slowdown, sw_thermal_slowdown, sw_power_cap)."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason bits: hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+    NVML_BITS = (0x8, 0x40, 0x20, 0x4)
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
+        self.thread = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu}.csv")
 
+    def _nvml_loop(self, nv, h):
+        import time
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                flags = ["Active" if bits & b else "Not Active" for b in self.NVML_BITS]
+                self.fh.write(f"{self.gpu}, {sm}, {mx}, {pw:.1f}, {bits:#x}, " + ", ".join(flags) + "\n")
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.01)
+
     def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        self.fh = open(self.path, "w")
         try:
-            os.makedirs(os.path.dirname(self.path), exist_ok=True)
-            self.fh = open(self.path, "w")
+            import threading
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.thread.start()
+            return self
+        except Exception:  # noqa: BLE001
+            self.thread = None
+        try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
@@ -113,17 +145,20 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
+        if self.thread:
+            self.stop.set()
+            self.thread.join(timeout=5)
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:  # noqa: BLE001
                 self.proc.kill()
-            self.fh.close()
+        self.fh.close()
 
     def summary(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        if not self.proc and not self.thread:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml / nvidia-smi unavailable"]}
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         with open(self.path) as f:

@@ -147,6 +147,8 @@ cudaError_t launch(const Geo& g, Prepared pr, const void* A, void* B, cudaStream
       pr.rp.A = A;
       pr.rp.B = B;
       return launch_rt(g.ka, g.kb, pr.spec.w1, pr.spec.w2, pr.mode, pr.rp, pr.l, s);
+    case kTma:
+      return launch_tma(g.ka, g.kb, pr.mode, pr.tp, A, B, pr.l, s);
     default:
       pr.sp.A = A;
       pr.sp.B = B;
@@ -167,7 +169,7 @@ int execute(ttb_plan_s* pl, const Prepared& pr0, const void* A, void* B, cudaStr
   if (!aligned(A, pr->a_align)) return fail(TTB_EINVAL, "A buffer: misaligned for its element kind");
   if (!aligned(B, pr->b_align)) return fail(TTB_EINVAL, "B buffer: misaligned for its element kind");
   Prepared run = *pr;
-  run.cp.sc = run.rp.sc = run.sp.sc = Scale{alpha, beta};
+  run.cp.sc = run.rp.sc = run.sp.sc = run.tp.sc = Scale{alpha, beta};
   const cudaError_t e = launch(pl->geo, run, A, B, s);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return ok();
@@ -741,7 +743,7 @@ int ttb_plan_describe(ttb_plan plan, char* buf, size_t len) {
   if (!plan) return fail(TTB_EINVAL, "plan: null handle");
   // the plan text plus the kernel that runs it (informational "fn" key)
   const Prepared& p = plan->prep;
-  const char* fn = p.spec.v == kRt ? "rt" : p.spec.v == kCopy ? (p.cp.long_rows ? "copy_rows" : "copy")
+  const char* fn = p.spec.v == kTma ? "tma" : p.spec.v == kRt ? "rt" : p.spec.v == kCopy ? (p.cp.long_rows ? "copy_rows" : "copy")
                    : p.sp.dense == 5 ? (p.sp.ly ? "btile" : "btile_lin") : p.sp.dense == 4 ? "vtile" : p.sp.dense >= 2 ? "dense" : p.sp.dense == 1 ? "tile" : "smem";
   const std::string t = p.spec.text() + ";fn=" + fn;
   if (!buf || len <= t.size()) return fail(TTB_EINVAL, "describe: buffer too small");

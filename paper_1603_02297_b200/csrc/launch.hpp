@@ -38,6 +38,12 @@ int occupancy_btile_big(int ka, int kb, int mode, int jy, int block, int smem);
 // leaves it zeroed); null if it cannot be allocated (static tile order)
 unsigned int* btile_counter(cudaStream_t s);
 
+// tma_kernel (Variant kTma, tensor maps encoded per launch from A and B), kern_tma.cu
+cudaError_t launch_tma(int ka, int kb, int mode, const TmaPlan& p, const void* A, void* B, const Launch& l,
+                       cudaStream_t s);
+int occupancy_tma(int ka, int kb, int mode, bool runs, int block, int smem);
+bool tma_available();
+
 // data utilities (util.cu)
 struct BoxParams {
   int rank = 0;

@@ -47,7 +47,7 @@ struct Space {
   int64_t sb[kSpaceDims];
 };
 
-enum Variant : int { kCopy = 0, kRt = 1, kSmem = 2 };
+enum Variant : int { kCopy = 0, kRt = 1, kSmem = 2, kTma = 3 };
 
 // Element-wise update constants (the W-typed alpha/beta are formed in-kernel).
 struct Scale {
@@ -132,6 +132,46 @@ struct SmemParams {
   uint32_t xp, xm;         // dense == 5, linear walk: X0 extent and tx / xp (xp 0: natural column order)
   Div32 dxm;               // divisor xm
 };
+
+// kTma: the tensor-map tile (tma.cuh).  One TMA box per tile and side: the A
+// tile [by][bx] (x fastest) is loaded from A's map, transposed through shared
+// memory into the B tile [bx][by], and stored through B's map (with beta != 0
+// the B tile is first loaded through the same map).  Each map is the tensor
+// seen from one side: its dims are the tile's axes with box > 1 (runs that are
+// contiguous in that tensor merged) plus one "carrier" dim that takes every
+// axis the tile covers with extent 1, folded as coordinate multiples (a
+// larger stride is always a whole multiple of the smallest one).
+constexpr int kTmaMaxRank = 5;
+constexpr int kTmaLevels = 12;
+constexpr int kTmaMaxStages = 8;
+struct TmaView {
+  int rank = 0;
+  int esz = 4;                 // map element bytes (4 or 8; 16-byte kinds as 2 x 8)
+  uint64_t dim[kTmaMaxRank];   // elements
+  uint64_t stride[kTmaMaxRank];  // bytes (stride[0] unused)
+  uint32_t box[kTmaMaxRank];
+};
+struct TmaPlan {
+  TmaView va, vb;
+  Scale sc;
+  uint32_t bx, by;          // tile extents along X / Y (flattened, OOB included)
+  uint32_t S;               // case 1: shared stride-1 run per (x, y) (1 in case 2)
+  uint32_t items;           // tiles
+  int nlev;                 // tile-index levels (mixed radix, first fastest)
+  Div32 lev[kTmaLevels];
+  int dimA[kTmaLevels], dimB[kTmaLevels];  // map dim a level's digit feeds
+  int32_t mulA[kTmaLevels], mulB[kTmaLevels];
+  uint32_t ns;              // ring stages
+  uint32_t tile_a, tile_b;  // bytes of one A / B tile in shared memory (128-B rounded)
+  // case 2: micro-tiles per tile and warp tiles (2^wxl x 2^(5-wxl) micro-tiles each)
+  uint32_t mx, my, nwx, nwt, wxl;
+  Div32 dnwx;
+  // case 1: 16-byte chunks per run, divisors for the (chunk, y, x) walk
+  uint32_t kch;
+  Div32 dk, dby;
+};
+constexpr int kTmaConsumerWarps = 4;
+constexpr int kTmaStoreWarps = 2;
 
 // btile_kernel warp roles: consumer warps write B; producer warps issue the
 // bulk copies (issued per warp through the uniform datapath, one lane's copy

@@ -537,6 +537,351 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
   }
 }
 
+// ----------------------------------------------------------- tensor maps --
+
+// Per-axis tile box of a TMA tile: the group's leading axes are covered
+// completely, the next one by `t / (their product)` elements (the partial
+// axis), later group axes by 1.  false when t is not of that form.
+bool tma_group_boxes(const Geo& g, const std::vector<int>& grp, int64_t t, int64_t* box) {
+  int64_t p = 1;
+  for (size_t i = 0; i < grp.size(); ++i) {
+    const int64_t n = g.n[grp[i]];
+    if (p * n >= t) {
+      if (t % p) return false;
+      box[grp[i]] = t / p;
+      return true;
+    }
+    box[grp[i]] = n;
+    p *= n;
+  }
+  return false;
+}
+
+// One side's tensor map: `tile` axes (view order, the first stride-1) each
+// get a dim unless they continue the previous dim in memory (then merged),
+// every other axis of the problem folds into one carrier dim.  Fills the
+// dim / multiplier each axis' tile digit feeds.
+bool tma_view(const Geo& g, const int64_t* st, int e, const std::vector<int>& tile, const int64_t* box,
+              TmaView* v, int* dim_of, int64_t* unit_of, const char** why) {
+  *v = TmaView{};
+  const int esz = e >= 8 ? 8 : 4;
+  const int64_t sub = e / esz;  // map elements per tensor element (2 for 16-byte kinds)
+  int64_t first_st[kTmaMaxRank] = {};
+  int last_axis = -1;
+  std::vector<bool> in_tile(static_cast<size_t>(g.r), false);
+  for (int a : tile) {
+    in_tile[static_cast<size_t>(a)] = true;
+    const int k = v->rank - 1;
+    if (k >= 0 && last_axis >= 0 && box[last_axis] == g.n[last_axis] &&
+        st[a] == st[last_axis] * g.n[last_axis] && static_cast<int64_t>(v->box[k]) * box[a] <= 256) {
+      v->dim[k] *= static_cast<uint64_t>(g.n[a]);
+      v->box[k] *= static_cast<uint32_t>(box[a]);
+    } else {
+      if (v->rank == kTmaMaxRank) {
+        *why = "tma: more than 5 dims";
+        return false;
+      }
+      const int nk = v->rank++;
+      v->dim[nk] = static_cast<uint64_t>(g.n[a]);
+      v->box[nk] = static_cast<uint32_t>(box[a]);
+      v->stride[nk] = static_cast<uint64_t>(st[a]) * static_cast<uint64_t>(e);
+      first_st[nk] = st[a];
+    }
+    dim_of[a] = v->rank - 1;
+    unit_of[a] = st[a] / first_st[v->rank - 1];
+    last_axis = a;
+  }
+  if (v->rank == 0 || st[tile[0]] != 1) {
+    *why = "tma: first dim not stride-1";
+    return false;
+  }
+  // the carrier: the uncovered axis with the smallest stride
+  int c = -1;
+  for (int a = 0; a < g.r; ++a)
+    if (!in_tile[static_cast<size_t>(a)] && (c < 0 || st[a] < st[c])) c = a;
+  if (c >= 0) {
+    if (v->rank == kTmaMaxRank) {
+      *why = "tma: more than 5 dims";
+      return false;
+    }
+    const int nk = v->rank++;
+    uint64_t ext = 1;
+    for (int a = 0; a < g.r; ++a) {
+      if (in_tile[static_cast<size_t>(a)]) continue;
+      if (st[a] % st[c]) {
+        *why = "tma: carrier stride does not divide";
+        return false;
+      }
+      dim_of[a] = nk;
+      unit_of[a] = st[a] / st[c];
+      ext += static_cast<uint64_t>(g.n[a] - 1) * static_cast<uint64_t>(unit_of[a]);
+    }
+    v->dim[nk] = ext;
+    v->box[nk] = 1;
+    v->stride[nk] = static_cast<uint64_t>(st[c]) * static_cast<uint64_t>(e);
+  }
+  v->esz = esz;
+  v->dim[0] *= static_cast<uint64_t>(sub);
+  v->box[0] *= static_cast<uint32_t>(sub);
+  for (int a = 0; a < g.r; ++a)
+    if (dim_of[a] == 0) unit_of[a] *= sub;
+  for (int k = 0; k < v->rank; ++k) {
+    if (v->box[k] < 1 || v->box[k] > 256) {
+      *why = "tma: box side outside 1..256";
+      return false;
+    }
+    if (v->dim[k] >= (uint64_t{1} << 31)) {
+      *why = "tma: dim extent beyond int32 coordinates";
+      return false;
+    }
+    if (k && (v->stride[k] % 16 || v->stride[k] >= (uint64_t{1} << 40))) {
+      *why = "tma: stride not a multiple of 16 bytes";
+      return false;
+    }
+  }
+  if ((static_cast<uint64_t>(v->box[0]) * static_cast<uint64_t>(esz)) % 16) {
+    *why = "tma: inner box not a multiple of 16 bytes";
+    return false;
+  }
+  return true;
+}
+
+// the launch-independent part of a TMA plan (false with a reason if the
+// spec does not apply to the problem)
+bool build_tma(const Geo& g, const Spec& s, TmaPlan* tp, std::string* why) {
+  const char* w = nullptr;
+  auto fail = [&](const char* m) {
+    if (why) *why = m;
+    return false;
+  };
+  const bool shared = g.pos[0] == 0;
+  const int start = shared ? 1 : 0;
+  if (g.r <= start) return fail("tma: nothing to transpose");
+  if (shared && g.ka != g.kb) return fail("tma: shared-run tiles need equal kinds");
+  const int64_t S = shared ? g.n[0] : 1;
+  if (shared && (S * g.eA) % 16) return fail("tma: shared run not a multiple of 16 bytes");
+  if (s.kx < 1 || s.ky < 1 || start + s.kx > g.r || start + s.ky > g.r) return fail("tma: bad groups");
+  const std::vector<int> xs = x_group(start, s.kx), ys = y_group(g, start, s.ky);
+  if (!disjoint(xs, ys)) return fail("tma: X/Y groups overlap");
+  int64_t box[kMaxRank];
+  for (int a = 0; a < g.r; ++a) box[a] = 1;
+  if (shared) box[0] = S;
+  if (s.tx < 1 || s.ty < 1 || !tma_group_boxes(g, xs, s.tx, box) || !tma_group_boxes(g, ys, s.ty, box))
+    return fail("tma: tile sides are not (whole leading axes) x (part of the next)");
+  std::vector<int> ta, tb;  // tile axes in A view / B view order
+  if (shared) {
+    ta.push_back(0);
+    tb.push_back(0);
+  }
+  auto covered = [&](const std::vector<int>& grp, std::vector<int>* out) {
+    int64_t p = 1;
+    for (int a : grp) {
+      out->push_back(a);
+      p *= box[a];
+      if (box[a] < g.n[a]) break;
+    }
+    return p;
+  };
+  std::vector<int> xt, yt;
+  const int64_t BX = covered(xs, &xt), BY = covered(ys, &yt);
+  ta.insert(ta.end(), xt.begin(), xt.end());
+  ta.insert(ta.end(), yt.begin(), yt.end());
+  tb.insert(tb.end(), yt.begin(), yt.end());
+  tb.insert(tb.end(), xt.begin(), xt.end());
+  TmaPlan& t = *tp;
+  t = TmaPlan{};
+  int dimA[kMaxRank], dimB[kMaxRank];
+  int64_t unitA[kMaxRank], unitB[kMaxRank];
+  if (!tma_view(g, g.sa, g.eA, ta, box, &t.va, dimA, unitA, &w) ||
+      !tma_view(g, g.sb, g.eB, tb, box, &t.vb, dimB, unitB, &w))
+    return fail(w);
+  t.sc = Scale{g.alpha, g.beta};
+  t.bx = static_cast<uint32_t>(BX);
+  t.by = static_cast<uint32_t>(BY);
+  t.S = static_cast<uint32_t>(S);
+  // tile-index levels: the partial axes of X and Y (order: which first), then
+  // every other axis not covered completely, in B order
+  std::vector<int> lev;
+  auto part = [&](const std::vector<int>& grp) {
+    for (int a : grp)
+      if (box[a] < g.n[a]) {
+        lev.push_back(a);
+        return;
+      }
+  };
+  if (s.order & 1) {
+    part(ys);
+    part(xs);
+  } else {
+    part(xs);
+    part(ys);
+  }
+  for (int k = 0; k < g.r; ++k) {
+    const int a = g.at[k];
+    if (box[a] < g.n[a] && std::find(lev.begin(), lev.end(), a) == lev.end()) lev.push_back(a);
+  }
+  if (static_cast<int>(lev.size()) > kTmaLevels) return fail("tma: too many tile levels");
+  uint64_t items = 1;
+  t.nlev = static_cast<int>(lev.size());
+  for (int l = 0; l < t.nlev; ++l) {
+    const int a = lev[static_cast<size_t>(l)];
+    const int64_t ext = (g.n[a] + box[a] - 1) / box[a];
+    items *= static_cast<uint64_t>(ext);
+    t.lev[l] = Div32::make(static_cast<uint32_t>(ext));
+    const int64_t ma = unitA[a] * box[a], mb = unitB[a] * box[a];
+    if (ma >= (int64_t{1} << 31) || mb >= (int64_t{1} << 31)) return fail("tma: coordinate step beyond int32");
+    t.dimA[l] = dimA[a];
+    t.dimB[l] = dimB[a];
+    t.mulA[l] = static_cast<int32_t>(ma);
+    t.mulB[l] = static_cast<int32_t>(mb);
+  }
+  if (items >= kIdxLimit) return fail("tma: too many tiles");
+  t.items = static_cast<uint32_t>(items);
+  const auto r128 = [](int64_t v) { return static_cast<uint32_t>((v + 127) & ~int64_t{127}); };
+  t.tile_a = r128(BX * BY * S * g.eA);
+  t.tile_b = r128(BX * BY * S * g.eB);
+  if (s.st < 2 || s.st > kTmaMaxStages) return fail("tma: stages outside 2..8");
+  t.ns = static_cast<uint32_t>(s.st);
+  const int64_t smem = static_cast<int64_t>(t.ns) * (t.tile_a + t.tile_b);
+  if (smem > 224 * 1024) return fail("tma: stages do not fit shared memory");
+  t.kch = 0;
+  t.mx = t.my = t.nwx = t.nwt = 0;
+  t.dnwx = Div32::make(1);
+  t.dk = t.dby = Div32::make(1);
+  if (shared) {
+    t.kch = static_cast<uint32_t>(S * g.eA / 16);
+    t.dk = Div32::make(t.kch);
+    t.dby = Div32::make(t.by);
+  } else {
+    const int wm = std::max(1, 16 / std::min(g.eA, g.eB));
+    if (BX % wm || BY % wm) return fail("tma: tile sides not multiples of the micro-tile");
+    t.mx = static_cast<uint32_t>(BX / wm);
+    t.my = static_cast<uint32_t>(BY / wm);
+    // warp tiles of 4 x 8 micro-tiles (the conflict-free lane map), or wider
+    // ones when the tile is short along y (fewer idle lanes)
+    t.wxl = 2;
+    auto util = [&](uint32_t l) {
+      const uint32_t wx = 1u << l, wy = 32u >> l;
+      return static_cast<double>(t.mx) * t.my / (((t.mx + wx - 1) / wx) * wx * (((t.my + wy - 1) / wy) * wy));
+    };
+    for (uint32_t l : {3u, 4u, 5u})
+      if (util(l) > util(t.wxl) * 1.25) t.wxl = l;
+    t.nwx = (t.mx + (1u << t.wxl) - 1) >> t.wxl;
+    t.nwt = t.nwx * ((t.my + (32u >> t.wxl) - 1) / (32u >> t.wxl));
+    t.dnwx = Div32::make(t.nwx);
+  }
+  return true;
+}
+
+bool prepare_tma(const Geo& g, const Spec& s, int sms, Prepared* p, std::string* why) {
+  if (!build_tma(g, s, &p->tp, why)) return false;
+  if (!tma_available()) {
+    if (why) *why = "tma: no tensor-map encoder in the driver";
+    return false;
+  }
+  const TmaPlan& t = p->tp;
+  const bool shared = t.kch > 0;
+  const int64_t smem = static_cast<int64_t>(t.ns) * (t.tile_a + t.tile_b);
+  p->l.smem = static_cast<int>(smem);
+  p->l.block = 32 * (kTmaConsumerWarps + 2 + kTmaStoreWarps);
+  const int occ_cap = s.occ > 0 ? s.occ : 64;
+  const int occ = std::min(occ_cap, std::max(1, occupancy_tma(g.ka, g.kb, g.mode, shared, p->l.block, p->l.smem)));
+  p->l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(t.items, int64_t{occ} * sms)));
+  p->a_align = 16;
+  p->b_align = 16;
+  return true;
+}
+
+// TMA tile candidates for every admissible (kx, ky): tile sides of the form
+// (whole leading axes) x (part of the next), the ones whose rows are an odd
+// number of 16-byte chunks first (conflict-free micro-tiles, tma.cuh)
+void tma_candidates(const Geo& g, std::vector<Spec>* out) {
+  const bool shared = g.pos[0] == 0;
+  const int start = shared ? 1 : 0;
+  if (g.r <= start) return;
+  const int64_t S = shared ? g.n[0] : 1;
+  if (shared && (g.ka != g.kb || (S * g.eA) % 16)) return;
+  const int wm = shared ? 1 : std::max(1, 16 / std::min(g.eA, g.eB));
+  const int y_first = g.at[start];
+  std::vector<Spec> c;
+  auto sides = [&](const std::vector<int>& grp, int e) {
+    std::vector<int64_t> v;
+    int64_t p = 1;
+    for (int a : grp) {
+      const int64_t n = g.n[a];
+      for (int64_t b = 1; b <= n; ++b) {
+        const int64_t t = p * b;
+        if (t > 1024 || b > 256) break;
+        if (t % wm) continue;
+        if (b != n && b % 4 != 0 && b * 2 < n) continue;  // keep the list short: multiples of 4 and the near-whole
+        v.push_back(t);
+      }
+      if (p * n > 1024 || n > 256) break;
+      p *= n;
+    }
+    (void)e;
+    return v;
+  };
+  for (int kx = 1; start + kx <= g.r && kx <= 3; ++kx) {
+    const std::vector<int> xs = x_group(start, kx);
+    if (std::find(xs.begin(), xs.end(), y_first) != xs.end()) break;
+    for (int ky = 1; start + ky <= g.r && ky <= 3; ++ky) {
+      const std::vector<int> ys = y_group(g, start, ky);
+      if (!disjoint(xs, ys)) break;
+      const bool xd = x_dense_in_a(g, xs, S), yd = y_dense_in_b(g, ys, S);
+      for (int64_t tx : sides(xs, g.eA)) {
+        for (int64_t ty : sides(ys, g.eB)) {
+          const int64_t tile = S * tx * ty * (g.eA + g.eB);
+          if (tile > 72 * 1024 || tile < 4 * 1024) continue;
+          int64_t box[kMaxRank];
+          for (int a = 0; a < g.r; ++a) box[a] = 1;
+          if (!tma_group_boxes(g, xs, tx, box) || !tma_group_boxes(g, ys, ty, box)) continue;
+          double eff = 1.0;
+          for (int a : xs)
+            if (box[a] < g.n[a]) {
+              eff *= static_cast<double>(g.n[a]) / (((g.n[a] + box[a] - 1) / box[a]) * box[a]);
+              break;
+            }
+          for (int a : ys)
+            if (box[a] < g.n[a]) {
+              eff *= static_cast<double>(g.n[a]) / (((g.n[a] + box[a] - 1) / box[a]) * box[a]);
+              break;
+            }
+          const int64_t run_a = S * (xd ? tx : g.n[xs[0]]) * g.eA, run_b = S * (yd ? ty : g.n[ys[0]]) * g.eB;
+          auto run_cost = [](int64_t r) { return r < 64 ? 4.0 : r < 128 ? 2.0 : r < 256 ? 0.7 : r < 512 ? 0.2 : 0.0; };
+          const bool odd = shared || (((tx * g.eA / 16) & 1) && ((ty * g.eB / 16) & 1));
+          Spec sp;
+          sp.v = kTma;
+          sp.kx = kx;
+          sp.ky = ky;
+          sp.tx = static_cast<int>(tx);
+          sp.ty = static_cast<int>(ty);
+          // stages: about 100 KB in flight per SM
+          sp.st = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(kTmaMaxStages, (200 * 1024) / tile)));
+          TmaPlan probe;
+          if (!build_tma(g, sp, &probe, nullptr)) continue;
+          sp.cost = 1.5 + (1.0 - eff) * 12.0 + run_cost(run_a) + run_cost(run_b) + (odd ? 0.0 : 0.6) +
+                    std::fabs(std::log2(static_cast<double>(tile) / (48.0 * 1024))) * 0.2 + 0.05 * (kx + ky);
+          c.push_back(sp);
+        }
+      }
+    }
+  }
+  std::stable_sort(c.begin(), c.end(), [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
+  int n = 0;
+  for (const Spec& sp : c) {
+    if (n >= 6) break;
+    out->push_back(sp);
+    if (n < 2) {
+      Spec o = sp;
+      o.order = 1;
+      o.cost += 0.01;
+      out->push_back(o);
+    }
+    ++n;
+  }
+}
+
 }  // namespace
 
 Geo make_geo(const Problem& m) {
@@ -575,6 +920,10 @@ std::string Spec::text() const {
       std::snprintf(buf, sizeof buf, "kern=rt;mx=%d;my=%d;lx=%d;kx=%d;ky=%d;order=%d;occ=%d", w1,
                     w2, lx, kx, ky, order, occ);
       break;
+    case kTma:
+      std::snprintf(buf, sizeof buf, "kern=tma;kx=%d;ky=%d;tx=%d;ty=%d;order=%d;occ=%d;st=%d", kx, ky, tx, ty,
+                    order, occ, st);
+      break;
     default:
       std::snprintf(buf, sizeof buf,
                     "kern=smem;kx=%d;ky=%d;tx=%d;ty=%d;order=%d;occ=%d;st=%d;bp=%d;vec=%d", kx, ky, tx,
@@ -604,6 +953,8 @@ bool Spec::parse(const std::string& s, Spec* out) {
         p.v = kRt;
       else if (v == "smem")
         p.v = kSmem;
+      else if (v == "tma")
+        p.v = kTma;
       else
         return false;
       continue;
@@ -745,6 +1096,8 @@ std::vector<Spec> candidates(const Geo& g) {
 
   // --- shared-memory staged tile (always applicable)
   smem_candidates(g, shared, &out);
+  // --- tensor-map tile (where every stride is a multiple of 16 bytes)
+  tma_candidates(g, &out);
   std::stable_sort(out.begin(), out.end(),
                    [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
   // the tile order alternative of the best two transposing candidates of
@@ -789,10 +1142,10 @@ std::vector<Spec> candidates(const Geo& g) {
   // register-transpose candidates survive even when staged tiles rank higher
   if (out.size() > 56) {
     std::vector<Spec> kept(out.begin(), out.begin() + 56);
-    for (Variant v : {kCopy, kRt}) {
+    for (Variant v : {kCopy, kRt, kTma}) {
       int have = 0;
       for (const Spec& k : kept) have += k.v == v;
-      for (size_t i = 56; i < out.size() && have < 4; ++i)
+      for (size_t i = 56; i < out.size() && have < (v == kTma ? 8 : 4); ++i)
         if (out[i].v == v) {
           kept.push_back(out[i]);
           ++have;
@@ -814,6 +1167,11 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     if (why) *why = m;
     return false;
   };
+  if (s.v == kTma) {
+    if (!prepare_tma(g, s, sms, &p, why)) return false;
+    *out = p;
+    return true;
+  }
   if (s.v == kCopy) {
     if (g.pos[0] != 0) return fail("copy: stride-1 index is transposed");
     const int v = s.w1;

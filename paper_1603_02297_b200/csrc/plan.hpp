@@ -59,6 +59,7 @@ struct Prepared {
   CopyParams cp{};
   RtParams rp{};
   SmemParams sp{};
+  TmaPlan tp{};
   int a_align = 1, b_align = 1;  // required base alignment (bytes) of A and B
 };
 

@@ -306,12 +306,33 @@ def reference_rows(slab_div: int, max_rows=None):
     return rows
 
 
-def time_reference(slab_div: int, steps: int, warmup: int, threads: int, max_rows=None,
-                   pick_best=True):
-    """Reference CPU path on host cores; returns (GB/s, seconds/step, sample text)."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+REF_SLAB_DIV = 16     # bounded sample: the leading 1/16 slab of every row
+REF_TUNE_CAP = 8      # capped tune queue, prefetch distances {0, 5}
+
+
+def time_reference(slab_div: int, steps: int, warmup: int, threads: int, max_rows=None):
+    """The reference's best CPU path, per row: its B-linear nest
+    (reference_transpose, executor.cpp:283-313) and execute_plan with the
+    winner of its own tune over a capped queue (tuner.cpp:221-244 over
+    build_candidates, search.cpp:243-303: max_implementations 8, prefetch
+    distances {0, 5}), whichever is faster, on all host threads.  One code
+    path for the --impl reference arm and the engine arm's cpu_baseline leg.
+    Returns (GB/s, seconds per step, sample text)."""
     orc = _oracle()
     ref, co = orc.RefOracle(), orc.COracle()
     sessions = []
+    n_plan = 0
     for w, origin, ext in reference_rows(slab_div, max_rows):
         s = orc.RefSession(ref, w.kind, w.kind, w.perm, ext, None, None, w.alpha, w.beta,
                            merge=True)
@@ -325,17 +346,15 @@ def time_reference(slab_div: int, steps: int, warmup: int, threads: int, max_row
         n = _prod(ext)
         nbytes = n * {"s": 4, "d": 8, "c": 8, "z": 16}[w.kind] * (3 if w.beta else 2)
         plan = None
-        if pick_best:
-            # the reference's best CPU path per row: its B-linear nest or its
-            # heuristic top-1 tuned plan (build_candidates + tune, capped at 1)
-            t_nest = min(s.run(threads) for _ in range(2))
-            try:
-                top1, _ = s.tune(threads, max_impl=1, warmups=0, reps=1)
-                t_plan = min(s.run(threads, top1) for _ in range(2))
-                if t_plan < t_nest:
-                    plan = top1
-            except Exception:  # noqa: BLE001
-                pass
+        t_nest = min(s.run(threads) for _ in range(2))
+        try:
+            best, _ = s.tune(threads, max_impl=REF_TUNE_CAP, warmups=1, reps=3)
+            t_plan = min(s.run(threads, best) for _ in range(2))
+            if t_plan < t_nest:
+                plan = best
+                n_plan += 1
+        except Exception:  # noqa: BLE001
+            pass
         sessions.append((s, plan, nbytes))
     for _ in range(warmup):
         for s, plan, _ in sessions:
@@ -349,7 +368,9 @@ def time_reference(slab_div: int, steps: int, warmup: int, threads: int, max_row
     total_bytes = sum(b for _, _, b in sessions)
     sec = statistics.median(per_step)
     sample = (f"every c5 row, leading 1/{slab_div} slab of B's outermost index, "
-              f"{len(sessions)} sub-problems, {total_bytes / 1e9:.2f} GB/step")
+              f"{len(sessions)} sub-problems, {total_bytes / 1e9:.2f} GB/step; per row the faster of "
+              f"reference_transpose and execute_plan(tune cap {REF_TUNE_CAP}, d in {{0,5}}) "
+              f"({n_plan} rows took the tuned plan); median of {steps} steps")
     for s, _, _ in sessions:
         s.close()
     return total_bytes / 1e9 / sec, sec, sample
@@ -363,7 +384,7 @@ def run_reference_arm(args):
     try:
         if not _oracle().have_ref():
             raise FileNotFoundError("oracle/_ref/libttune_ref.so not built")
-        gbs, sec, sample = time_reference(16, args.steps, args.warmup, threads)
+        gbs, sec, sample = time_reference(REF_SLAB_DIV, args.steps, args.warmup, threads)
     except Exception as e:  # noqa: BLE001
         print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}))
         return 0
@@ -374,7 +395,7 @@ def run_reference_arm(args):
         "data": "synthetic (seeded counter-based generator, SURVEY s8(d))",
         "config": config_block(args.gpus), "impl": "reference",
         "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads,
-                         "kind": "reference", "sample": sample},
+                         "kind": "reference", "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -566,7 +587,7 @@ def run_engine_arm(args):
         r.free()
     torch.cuda.empty_cache()
     # end-to-end through the public API with pinned host buffers
-    e2e = None if args.no_e2e else run_e2e(torch, ttb, rows, world, allmax, steps=min(args.steps, 2))
+    e2e = None if args.no_e2e else run_e2e(torch, ttb, rows, world, allmax, steps=min(args.steps, 3))
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
@@ -585,19 +606,55 @@ def run_engine_arm(args):
             line["configs"] = bench_configs(torch, ttb, peak, d2d)
         if not args.no_cpu:
             try:
-                kind = "reference" if _oracle().have_ref() else "port"
-                gbs, sec, sample = time_reference(32, 1, 0, os.cpu_count() or 1, pick_best=False)
+                if not _oracle().have_ref():
+                    raise FileNotFoundError("oracle/_ref/libttune_ref.so not built")
+                gbs, sec, sample = time_reference(REF_SLAB_DIV, 3, 1, os.cpu_count() or 1)
                 line["cpu_baseline"] = {"value": round(gbs, 3), "unit": "GB/s",
-                                        "cores": os.cpu_count() or 1, "kind": kind,
-                                        "sample": sample + " (reference_transpose)"}
+                                        "cores": os.cpu_count() or 1, "kind": "reference",
+                                        "cpu_model": cpu_model(), "sample": sample}
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": 0,
                                         "kind": "reference", "sample": f"failed: {e}"}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     return 0
+
+
+def measure_pcie(torch, nbytes=1 << 30):
+    """Pinned host <-> device copy bandwidth (GB/s): H2D alone, D2H alone, and
+    both at once on two streams (PCIe is full duplex) -- the e2e roofline."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn, reps=3):
+        best = 1e30
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    t_h2d = timed(lambda: d.copy_(h, non_blocking=True))
+    t_d2h = timed(lambda: h2.copy_(d2, non_blocking=True))
+
+    def both():
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+
+    t_both = timed(both)
+    del h, h2, d, d2
+    torch.cuda.empty_cache()
+    return {"h2d_gbs": round(nbytes / 1e9 / t_h2d, 1), "d2h_gbs": round(nbytes / 1e9 / t_d2h, 1),
+            "both_gbs": round(2 * nbytes / 1e9 / t_both, 1)}
 
 
 def run_e2e(torch, ttb, rows, world, allmax, steps):
@@ -652,9 +709,19 @@ def run_e2e(torch, ttb, rows, world, allmax, steps):
     per_step = allmax(total / steps)
     nbytes = sum(w.algorithmic_bytes for w in {id(r.w): r.w for r in rows}.values())
     del host_a, host_b
-    return {"value": round(nbytes / 1e9 / per_step, 3), "unit": "GB/s",
+    torch.cuda.empty_cache()
+    # PCIe roofline: both directions overlapped at the measured duplex rate
+    # (each direction at half of it), or one direction alone, whichever is slower
+    pcie = measure_pcie(torch)
+    half = pcie["both_gbs"] / 2
+    t_min = max(h2d / 1e9 / min(half, pcie["h2d_gbs"]), d2h / 1e9 / min(half, pcie["d2h_gbs"]))
+    roof = nbytes / 1e9 / t_min if t_min > 0 else None
+    value = nbytes / 1e9 / per_step
+    return {"value": round(value, 3), "unit": "GB/s",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "ms_per_step": round(per_step * 1e3, 2),
+            "ms_per_step": round(per_step * 1e3, 2), "steps": steps,
+            "pcie": dict(pcie, roof_gbs=round(roof, 1) if roof else None,
+                         frac=round(value / roof, 3) if roof else None),
             "path": "GpuPlan.execute_host (ttb_plan_execute_host), pinned host buffers"}
 
 
@@ -671,9 +738,39 @@ def main():
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")
         args.warmup = 3
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        return spawn_ranks(args.gpus)
+    if world is not None and int(world) != args.gpus:
+        log(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
+        return 2
+    if args.gpus > 1:
+        # the communicator's init lines (nranks) in the log of every rank
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_engine_arm(args)
+
+
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` outside torchrun: start N ranks of this command on this node
+    (the torchrun environment: RANK / LOCAL_RANK / WORLD_SIZE / MASTER_*),
+    rank 0's stdout carries the JSON line; exit code = worst rank's."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, *sys.argv], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    return rc
 
 
 if __name__ == "__main__":

@@ -166,7 +166,8 @@ int ttb_plan_describe(ttb_plan plan, char* buf, size_t len);
 int ttb_plan_candidates(ttb_plan plan, char* buf, size_t len);
 /* force a candidate by its serialized text (TTB_EINVAL if not applicable) */
 int ttb_plan_select(ttb_plan plan, const char* plan_text);
-/* per-launch: number of kernel launches and the kernel names of one execute */
+/* kernel launches of one ttb_plan_execute: 1, or the number of < 2^31-element
+   boxes an oversized problem runs as */
 int ttb_plan_launches(ttb_plan plan, int* launches_per_execute);
 
 /* ------------------------------------------ persistent solution cache -- */

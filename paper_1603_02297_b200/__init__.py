@@ -428,9 +428,28 @@ class GpuPlan:
         except Exception:  # noqa: BLE001 -- interpreter shutdown
             pass
 
-    def execute(self, a, b, stream=None) -> None:
+    def _pointers(self, a, b):
+        """Device addresses of A and B.  TensorBuffers are checked like
+        execute_plan's check_buffers (executor.cpp:315-322): kind, then
+        capacity; torch tensors by byte capacity; raw integers are taken as
+        they are (the C ABI cannot size a bare pointer)."""
+        p = self.problem
+        for name, buf, kind, need in (("A", a, p.kind_a, required_elements_a(p)),
+                                      ("B", b, p.kind_b, required_elements_b(p))):
+            if isinstance(buf, TensorBuffer):
+                if buf.kind() != kind:
+                    raise ValueError(f"{name} buffer: element kind mismatch")
+                if buf.elements() < need:
+                    raise ValueError(f"{name} buffer: too small for problem")
+            elif hasattr(buf, "numel") and hasattr(buf, "element_size"):
+                if buf.numel() * buf.element_size() < need * kind.bytes:
+                    raise ValueError(f"{name} buffer: too small for problem")
         pa = a.data_ptr() if hasattr(a, "data_ptr") else int(a)
         pb = b.data_ptr() if hasattr(b, "data_ptr") else int(b)
+        return pa, pb
+
+    def execute(self, a, b, stream=None) -> None:
+        pa, pb = self._pointers(a, b)
         check(lib.ttb_plan_execute(self._h, C.c_void_p(pa), C.c_void_p(pb), _stream(stream)))
 
     def execute_host(self, a_host, b_host) -> None:
@@ -440,8 +459,7 @@ class GpuPlan:
         check(lib.ttb_plan_execute_host(self._h, C.c_void_p(pa), C.c_void_p(pb)))
 
     def autotune(self, a, b, warmups: int = 2, reps: int = 3, stream=None) -> str:
-        pa = a.data_ptr() if hasattr(a, "data_ptr") else int(a)
-        pb = b.data_ptr() if hasattr(b, "data_ptr") else int(b)
+        pa, pb = self._pointers(a, b)
         check(lib.ttb_plan_autotune(self._h, C.c_void_p(pa), C.c_void_p(pb), warmups, reps,
                                     _stream(stream)))
         return self.describe()
@@ -451,8 +469,7 @@ class GpuPlan:
         """pipeline.cpp:102-185 for this plan: select the cached plan of (canonical
         key, hardware key) from `cache_file`, or autotune and append the winner.
         Returns True on a cache hit.  B holds one application afterwards."""
-        pa = a.data_ptr() if hasattr(a, "data_ptr") else int(a)
-        pb = b.data_ptr() if hasattr(b, "data_ptr") else int(b)
+        pa, pb = self._pointers(a, b)
         hit = C.c_int(0)
         check(lib.ttb_plan_tune_cached(self._h, str(cache_file).encode(), C.c_void_p(pa),
                                        C.c_void_p(pb), warmups, reps, _stream(stream),
@@ -471,6 +488,12 @@ class GpuPlan:
 
     def select(self, text: str) -> None:
         check(lib.ttb_plan_select(self._h, text.encode()))
+
+    def launches(self) -> int:
+        """Kernel launches per execute (one per box for oversized problems)."""
+        n = C.c_int(0)
+        check(lib.ttb_plan_launches(self._h, C.byref(n)))
+        return n.value
 
 
 def execute_plan(p: TransposeProblem, plan: Optional[GpuPlan], a: TensorBuffer, b: TensorBuffer,

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -68,6 +69,15 @@ int current_device(int* dev, int* sms) {
 
 }  // namespace
 
+struct ttb_plan_s;
+
+// A box of an oversized problem: its element offsets in A and B and the plan
+// of its extents (same strides as the whole problem)
+struct SubBox {
+  int64_t off_a = 0, off_b = 0;
+  std::shared_ptr<ttb_plan_s> plan;
+};
+
 struct ttb_plan_s {
   Problem orig;
   Merged merged;
@@ -87,6 +97,9 @@ struct ttb_plan_s {
   cudaStream_t ds = nullptr;  // device->host copies (pipelined path)
   std::vector<cudaEvent_t> evs;
   std::unordered_map<int64_t, std::unique_ptr<ttb_plan_s>> chunk_plans;  // by slab extent
+  // problems whose A or B footprint reaches 2^31 elements run as boxes below
+  // that size (every kernel keeps 32-bit index spaces); empty otherwise
+  std::vector<SubBox> boxes;
   ~ttb_plan_s() {
     if (dA) cudaFree(dA);
     if (dB) cudaFree(dB);
@@ -103,7 +116,43 @@ namespace {
 
 std::mutex g_mu;
 std::unordered_map<std::string, std::string> g_choice;                 // key -> spec text
-std::unordered_map<std::string, std::unique_ptr<ttb_plan_s>> g_plans;  // one-shot API plans
+// one-shot API plans, shared: a caller keeps its plan alive while executing
+// even if an autotune elsewhere drops the cache (re-entrant)
+std::unordered_map<std::string, std::shared_ptr<ttb_plan_s>> g_plans;
+
+constexpr int64_t kBoxLimit = int64_t{1} << 31;
+
+// Halve the box along its largest-stride axis (of the side that is too big)
+// until both footprints are below 2^31 elements.
+void split_boxes(const Problem& m, std::vector<std::pair<std::vector<int64_t>, std::vector<int64_t>>>* out) {
+  const std::vector<int64_t> sa = m.a_strides(), sb = m.b_strides_of_a();
+  const int r = m.rank();
+  std::vector<std::pair<std::vector<int64_t>, std::vector<int64_t>>> work{
+      {std::vector<int64_t>(static_cast<size_t>(r), 0), m.sizes}};
+  while (!work.empty()) {
+    auto b = work.back();
+    work.pop_back();
+    int64_t fa = 1, fb = 1;
+    for (int a = 0; a < r; ++a) {
+      fa += (b.second[a] - 1) * sa[a];
+      fb += (b.second[a] - 1) * sb[a];
+    }
+    if (fa < kBoxLimit && fb < kBoxLimit) {
+      out->push_back(b);
+      continue;
+    }
+    const std::vector<int64_t>& st = fa >= kBoxLimit ? sa : sb;
+    int ax = -1;
+    for (int a = 0; a < r; ++a)
+      if (b.second[a] > 1 && (ax < 0 || st[a] > st[ax])) ax = a;
+    auto lo = b, hi = b;
+    lo.second[ax] = b.second[ax] / 2;
+    hi.first[ax] += lo.second[ax];
+    hi.second[ax] = b.second[ax] - lo.second[ax];
+    work.push_back(hi);
+    work.push_back(lo);
+  }
+}
 
 int build_plan(const Problem& p, int flags, std::unique_ptr<ttb_plan_s>* out) {
   auto pl = std::make_unique<ttb_plan_s>();
@@ -113,11 +162,43 @@ int build_plan(const Problem& p, int flags, std::unique_ptr<ttb_plan_s>* out) {
     return fail(TTB_EINVAL, "perm: rank " + std::to_string(pl->merged.p.rank()) +
                                 " after merging exceeds TTB_MAX_RANK");
   pl->geo = make_geo(pl->merged.p);
-  pl->cands = candidates(pl->geo);
   int rc = current_device(&pl->device, &pl->sms);
   if (rc) return rc;
   pl->key = cache_key(p) + "@dev" + std::to_string(pl->device);
   pl->cached = !(flags & TTB_PLAN_NO_CACHE);
+  if (pl->geo.foot_a >= kBoxLimit || pl->geo.foot_b >= kBoxLimit) {
+    // oversized: boxes of the merged problem, one plan per distinct extent
+    const Problem& m = pl->merged.p;
+    const std::vector<int64_t> sa = m.a_strides(), sb = m.b_strides_of_a();
+    std::vector<std::pair<std::vector<int64_t>, std::vector<int64_t>>> boxes;
+    split_boxes(m, &boxes);
+    std::map<std::vector<int64_t>, std::shared_ptr<ttb_plan_s>> by_ext;
+    for (const auto& b : boxes) {
+      std::shared_ptr<ttb_plan_s>& sub = by_ext[b.second];
+      if (!sub) {
+        Problem q = m;
+        q.sizes = b.second;
+        std::unique_ptr<ttb_plan_s> fresh;
+        rc = build_plan(q, flags | TTB_PLAN_NO_CACHE, &fresh);
+        if (rc) return rc;
+        sub = std::shared_ptr<ttb_plan_s>(std::move(fresh));
+      }
+      SubBox x;
+      for (int a = 0; a < m.rank(); ++a) {
+        x.off_a += b.first[a] * sa[a];
+        x.off_b += b.first[a] * sb[a];
+      }
+      x.plan = sub;
+      pl->boxes.push_back(x);
+    }
+    const ttb_plan_s& first = *pl->boxes.front().plan;
+    pl->cands = first.cands;
+    pl->prep = first.prep;
+    pl->fallback = first.fallback;
+    *out = std::move(pl);
+    return TTB_OK;
+  }
+  pl->cands = candidates(pl->geo);
   std::string why;
   bool have = false;
   if (pl->cached) {
@@ -164,6 +245,17 @@ int execute(ttb_plan_s* pl, const Prepared& pr0, const void* A, void* B, cudaStr
             double alpha, double beta) {
   if (!A) return fail(TTB_EINVAL, "A buffer: null pointer");
   if (!B) return fail(TTB_EINVAL, "B buffer: null pointer");
+  if (!pl->boxes.empty()) {
+    const size_t ea = static_cast<size_t>(kind_bytes(pl->orig.kind_a));
+    const size_t eb = static_cast<size_t>(kind_bytes(pl->orig.kind_b));
+    for (const SubBox& x : pl->boxes) {
+      const int rc = execute(x.plan.get(), x.plan->prep,
+                             static_cast<const char*>(A) + static_cast<size_t>(x.off_a) * ea,
+                             static_cast<char*>(B) + static_cast<size_t>(x.off_b) * eb, s, alpha, beta);
+      if (rc) return rc;
+    }
+    return ok();
+  }
   const Prepared* pr = &pr0;
   if (!aligned(A, pr->a_align) || !aligned(B, pr->b_align)) pr = &pl->fallback;
   if (!aligned(A, pr->a_align)) return fail(TTB_EINVAL, "A buffer: misaligned for its element kind");
@@ -512,11 +604,11 @@ int ttb_transpose(int kind_a, int kind_b, int rank, const int* perm, const int64
     if (rc) return rc;
     const int mode = p.beta != 0.0 ? 2 : (p.alpha == 1.0 ? 0 : 1);
     const std::string key = cache_key(p) + "@dev" + std::to_string(dev) + "|m" + std::to_string(mode);
-    ttb_plan_s* pl = nullptr;
+    std::shared_ptr<ttb_plan_s> pl;
     {
       std::lock_guard<std::mutex> lk(g_mu);
       auto it = g_plans.find(key);
-      if (it != g_plans.end()) pl = it->second.get();
+      if (it != g_plans.end()) pl = it->second;
     }
     if (!pl) {
       std::unique_ptr<ttb_plan_s> fresh;
@@ -524,10 +616,10 @@ int ttb_transpose(int kind_a, int kind_b, int rank, const int* perm, const int64
       if (rc) return rc;
       std::lock_guard<std::mutex> lk(g_mu);
       auto& slot = g_plans[key];
-      if (!slot) slot = std::move(fresh);
-      pl = slot.get();
+      if (!slot) slot = std::shared_ptr<ttb_plan_s>(std::move(fresh));
+      pl = slot;
     }
-    return execute(pl, pl->prep, A, B, reinterpret_cast<cudaStream_t>(stream), alpha, beta);
+    return execute(pl.get(), pl->prep, A, B, reinterpret_cast<cudaStream_t>(stream), alpha, beta);
   });
 }
 
@@ -573,6 +665,34 @@ int ttb_plan_autotune(ttb_plan plan, const void* A, void* B, int warmups, int re
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (warmups < 0 || reps < 1)
       return fail(TTB_EINVAL, "protocol: need warmups >= 0 and repetitions >= 1");
+    if (!plan->boxes.empty()) {
+      // oversized problem: tune the first box (one application on return),
+      // give its variant to every other box plan it applies to, and run the
+      // remaining boxes once so that B holds exactly one application
+      const size_t ea = static_cast<size_t>(kind_bytes(plan->orig.kind_a));
+      const size_t eb = static_cast<size_t>(kind_bytes(plan->orig.kind_b));
+      const SubBox& x0 = plan->boxes.front();
+      int rc = ttb_plan_autotune(x0.plan.get(), static_cast<const char*>(A) + static_cast<size_t>(x0.off_a) * ea,
+                                 static_cast<char*>(B) + static_cast<size_t>(x0.off_b) * eb, warmups, reps,
+                                 stream);
+      if (rc) return rc;
+      const Spec spec = x0.plan->prep.spec;
+      for (size_t i = 1; i < plan->boxes.size(); ++i) {
+        ttb_plan_s* sub = plan->boxes[i].plan.get();
+        Prepared pr;
+        if (sub != x0.plan.get() && prepare(sub->geo, spec, sub->sms, &pr, nullptr)) sub->prep = pr;
+      }
+      for (size_t i = 1; i < plan->boxes.size(); ++i) {
+        const SubBox& x = plan->boxes[i];
+        rc = execute(x.plan.get(), x.plan->prep, static_cast<const char*>(A) + static_cast<size_t>(x.off_a) * ea,
+                     static_cast<char*>(B) + static_cast<size_t>(x.off_b) * eb, s, plan->orig.alpha,
+                     plan->orig.beta);
+        if (rc) return rc;
+      }
+      plan->prep = x0.plan->prep;
+      plan->tuned_ms = x0.plan->tuned_ms * static_cast<float>(plan->boxes.size());
+      return ok();
+    }
     void* target = B;
     void* scratch = nullptr;
     cudaError_t e;
@@ -745,7 +865,8 @@ int ttb_plan_describe(ttb_plan plan, char* buf, size_t len) {
   const Prepared& p = plan->prep;
   const char* fn = p.spec.v == kTma ? "tma" : p.spec.v == kRt ? "rt" : p.spec.v == kCopy ? (p.cp.long_rows ? "copy_rows" : "copy")
                    : p.sp.dense == 5 ? (p.sp.ly ? "btile" : "btile_lin") : p.sp.dense == 4 ? "vtile" : p.sp.dense >= 2 ? "dense" : p.sp.dense == 1 ? "tile" : "smem";
-  const std::string t = p.spec.text() + ";fn=" + fn;
+  std::string t = p.spec.text() + ";fn=" + fn;
+  if (!plan->boxes.empty()) t += ";boxes=" + std::to_string(plan->boxes.size());
   if (!buf || len <= t.size()) return fail(TTB_EINVAL, "describe: buffer too small");
   std::memcpy(buf, t.c_str(), t.size() + 1);
   return ok();
@@ -767,6 +888,17 @@ int ttb_plan_select(ttb_plan plan, const char* plan_text) {
     if (!plan_text || !Spec::parse(plan_text, &s)) return fail(TTB_EINVAL, "plan: cannot parse plan text");
     std::string why;
     Prepared pr;
+    if (!plan->boxes.empty()) {  // every box plan it applies to (the first one must)
+      for (size_t i = 0; i < plan->boxes.size(); ++i) {
+        ttb_plan_s* sub = plan->boxes[i].plan.get();
+        if (prepare(sub->geo, s, sub->sms, &pr, &why))
+          sub->prep = pr;
+        else if (i == 0)
+          return fail(TTB_EINVAL, "plan: " + why);
+      }
+      plan->prep = plan->boxes.front().plan->prep;
+      return ok();
+    }
     if (!prepare(plan->geo, s, plan->sms, &pr, &why)) return fail(TTB_EINVAL, "plan: " + why);
     plan->prep = pr;
     return ok();
@@ -775,7 +907,8 @@ int ttb_plan_select(ttb_plan plan, const char* plan_text) {
 
 int ttb_plan_launches(ttb_plan plan, int* launches_per_execute) {
   if (!plan) return fail(TTB_EINVAL, "plan: null handle");
-  if (launches_per_execute) *launches_per_execute = 1;
+  // one kernel per execute, one per box for oversized problems
+  if (launches_per_execute) *launches_per_execute = plan->boxes.empty() ? 1 : static_cast<int>(plan->boxes.size());
   return ok();
 }
 

@@ -4,31 +4,56 @@
 // not through the ring), 1-16 column elements per consumer lane or the linear
 // walk (0).  Tiles of 32 KB and more run with twice the warps
 // (kern_btile_big.cu), selected by the launch's block size.
-#include <map>
+#include <atomic>
 #include <mutex>
-#include <utility>
 
 #include "btile_dispatch.cuh"
 
 namespace ttb {
 
-unsigned int* btile_counter(cudaStream_t s) {
+// Tile counters [next, done] for btile launches: a ring of slots per device,
+// each launch takes the next slot (a host-side atomic), so launches that run
+// at the same time -- other streams, other host threads on one stream handle
+// -- never share one; the kernel leaves its slot zeroed.  A graph launch
+// keeps the slot it was captured with (a graph exec never runs concurrently
+// with itself).  The ring is allocated by btile_counters_init() when a plan
+// is prepared (not during a stream capture); a launch that finds none falls
+// back to the static tile order.
+constexpr int kCounterSlots = 4096;
+constexpr int kMaxDevices = 64;
+std::atomic<unsigned int*> g_ring[kMaxDevices];
+std::atomic<uint32_t> g_next{0};
+
+void btile_counters_init() {
   static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, unsigned int*> counters;  // kept for the process
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+    cudaGetLastError();
+    return;
+  }
+  if (g_ring[dev].load()) return;
   std::lock_guard<std::mutex> lk(mu);
-  auto it = counters.find({dev, s});
-  if (it != counters.end()) return it->second;
+  if (g_ring[dev].load()) return;
   void* p = nullptr;
-  if (cudaMalloc(&p, 2 * sizeof(unsigned int)) != cudaSuccess ||
-      cudaMemset(p, 0, 2 * sizeof(unsigned int)) != cudaSuccess) {
+  if (cudaMalloc(&p, 2 * sizeof(unsigned int) * kCounterSlots) != cudaSuccess ||
+      cudaMemset(p, 0, 2 * sizeof(unsigned int) * kCounterSlots) != cudaSuccess) {
     cudaGetLastError();
     if (p) cudaFree(p);
+    return;
+  }
+  g_ring[dev].store(static_cast<unsigned int*>(p));
+}
+
+unsigned int* btile_counter(cudaStream_t) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+    cudaGetLastError();
     return nullptr;
   }
-  counters[{dev, s}] = static_cast<unsigned int*>(p);
-  return static_cast<unsigned int*>(p);
+  unsigned int* ring = g_ring[dev].load();
+  if (!ring) return nullptr;
+  const uint32_t slot = g_next.fetch_add(1) % kCounterSlots;
+  return ring + 2 * slot;
 }
 
 using BtileSmall = BtileCfg<kBtileConsumerWarps, kBtileProducerWarps, 0, 1, 2, 4, 8, 16>;

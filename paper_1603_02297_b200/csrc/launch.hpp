@@ -33,10 +33,11 @@ int occupancy_btile(int ka, int kb, int mode, int jy, int block, int smem);
 cudaError_t launch_btile_big(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                              cudaStream_t s);
 int occupancy_btile_big(int ka, int kb, int mode, int jy, int block, int smem);
-// btile_kernel's tile counter [next, done] for launches on stream s (one per
-// device and stream: launches on one stream never overlap, and the kernel
-// leaves it zeroed); null if it cannot be allocated (static tile order)
+// btile_kernel's tile counter [next, done] for one launch: the next slot of a
+// per-device ring (kern_btile.cu), or null before btile_counters_init() ran
+// on this device (static tile order)
 unsigned int* btile_counter(cudaStream_t s);
+void btile_counters_init();
 
 // tma_kernel (Variant kTma, tensor maps encoded per launch from A and B), kern_tma.cu
 cudaError_t launch_tma(int ka, int kb, int mode, const TmaPlan& p, const void* A, void* B, const Launch& l,

@@ -161,7 +161,7 @@ struct TmaPlan {
   Div32 lev[kTmaLevels];
   int dimA[kTmaLevels], dimB[kTmaLevels];  // map dim a level's digit feeds
   int32_t mulA[kTmaLevels], mulB[kTmaLevels];
-  uint32_t ns;              // ring stages
+  uint32_t ns, nsb;         // A ring / B ring slots
   uint32_t tile_a, tile_b;  // bytes of one A / B tile in shared memory (128-B rounded)
   // case 2: micro-tiles per tile and warp tiles (2^wxl x 2^(5-wxl) micro-tiles each)
   uint32_t mx, my, nwx, nwt, wxl;

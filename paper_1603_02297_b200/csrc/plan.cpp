@@ -26,6 +26,7 @@ bool build_space(const Geo& g, const std::vector<int>& axes, Space* s) {
   uint64_t tot = 1;
   for (size_t i = 0; i < axes.size(); ++i) {
     const int a = axes[i];
+    if (static_cast<uint64_t>(g.n[a]) >= kIdxLimit) return false;  // before it narrows
     s->ext[i] = Div32::make(static_cast<uint32_t>(g.n[a]));
     s->sa[i] = g.sa[a];
     s->sb[i] = g.sb[a];
@@ -695,6 +696,12 @@ bool build_tma(const Geo& g, const Spec& s, TmaPlan* tp, std::string* why) {
   if (!tma_view(g, g.sa, g.eA, ta, box, &t.va, dimA, unitA, &w) ||
       !tma_view(g, g.sb, g.eB, tb, box, &t.vb, dimB, unitB, &w))
     return fail(w);
+  // a TMA store clips the innermost dim at 16-byte granularity (measured on
+  // B200: the chunk holding a row's last element is written whole), so a
+  // partial tile along it needs rows that end on a 16-byte boundary --
+  // otherwise B's padding or the next row's first elements would be written
+  if (t.vb.dim[0] % t.vb.box[0] && (t.vb.dim[0] * static_cast<uint64_t>(t.vb.esz)) % 16)
+    return fail("tma: B rows end inside a 16-byte chunk and the tile is partial along them");
   t.sc = Scale{g.alpha, g.beta};
   t.bx = static_cast<uint32_t>(BX);
   t.by = static_cast<uint32_t>(BY);
@@ -727,6 +734,7 @@ bool build_tma(const Geo& g, const Spec& s, TmaPlan* tp, std::string* why) {
     const int a = lev[static_cast<size_t>(l)];
     const int64_t ext = (g.n[a] + box[a] - 1) / box[a];
     items *= static_cast<uint64_t>(ext);
+    if (items >= kIdxLimit) return fail("tma: too many tiles");
     t.lev[l] = Div32::make(static_cast<uint32_t>(ext));
     const int64_t ma = unitA[a] * box[a], mb = unitB[a] * box[a];
     if (ma >= (int64_t{1} << 31) || mb >= (int64_t{1} << 31)) return fail("tma: coordinate step beyond int32");
@@ -741,8 +749,11 @@ bool build_tma(const Geo& g, const Spec& s, TmaPlan* tp, std::string* why) {
   t.tile_a = r128(BX * BY * S * g.eA);
   t.tile_b = r128(BX * BY * S * g.eB);
   if (s.st < 2 || s.st > kTmaMaxStages) return fail("tma: stages outside 2..8");
+  const int nb = s.sb ? s.sb : s.st;
+  if (nb < 2 || nb > kTmaMaxStages) return fail("tma: B slots outside 2..8");
   t.ns = static_cast<uint32_t>(s.st);
-  const int64_t smem = static_cast<int64_t>(t.ns) * (t.tile_a + t.tile_b);
+  t.nsb = static_cast<uint32_t>(nb);
+  const int64_t smem = static_cast<int64_t>(t.ns) * t.tile_a + static_cast<int64_t>(t.nsb) * t.tile_b;
   if (smem > 224 * 1024) return fail("tma: stages do not fit shared memory");
   t.kch = 0;
   t.mx = t.my = t.nwx = t.nwt = 0;
@@ -781,7 +792,7 @@ bool prepare_tma(const Geo& g, const Spec& s, int sms, Prepared* p, std::string*
   }
   const TmaPlan& t = p->tp;
   const bool shared = t.kch > 0;
-  const int64_t smem = static_cast<int64_t>(t.ns) * (t.tile_a + t.tile_b);
+  const int64_t smem = static_cast<int64_t>(t.ns) * t.tile_a + static_cast<int64_t>(t.nsb) * t.tile_b;
   p->l.smem = static_cast<int>(smem);
   p->l.block = 32 * (kTmaConsumerWarps + 2 + kTmaStoreWarps);
   const int occ_cap = s.occ > 0 ? s.occ : 64;
@@ -856,8 +867,16 @@ void tma_candidates(const Geo& g, std::vector<Spec>* out) {
           sp.ky = ky;
           sp.tx = static_cast<int>(tx);
           sp.ty = static_cast<int>(ty);
-          // stages: about 100 KB in flight per SM
-          sp.st = static_cast<int>(std::max<int64_t>(2, std::min<int64_t>(kTmaMaxStages, (200 * 1024) / tile)));
+          // one CTA per SM with a deep A ring (loads in flight) and three B
+          // slots; the second form (two CTAs per SM) is added below
+          const int64_t ta = S * tx * ty * g.eA, tb = S * tx * ty * g.eB;
+          sp.sb = 3;
+          sp.st = static_cast<int>(std::min<int64_t>(kTmaMaxStages, (200 * 1024 - 3 * tb) / ta));
+          if (sp.st < 2) {
+            sp.sb = 2;
+            sp.st = static_cast<int>(std::min<int64_t>(kTmaMaxStages, (200 * 1024 - 2 * tb) / ta));
+          }
+          if (sp.st < 2) continue;
           TmaPlan probe;
           if (!build_tma(g, sp, &probe, nullptr)) continue;
           sp.cost = 1.5 + (1.0 - eff) * 12.0 + run_cost(run_a) + run_cost(run_b) + (odd ? 0.0 : 0.6) +
@@ -870,7 +889,7 @@ void tma_candidates(const Geo& g, std::vector<Spec>* out) {
   std::stable_sort(c.begin(), c.end(), [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
   int n = 0;
   for (const Spec& sp : c) {
-    if (n >= 6) break;
+    if (n >= 5) break;
     out->push_back(sp);
     if (n < 2) {
       Spec o = sp;
@@ -878,6 +897,14 @@ void tma_candidates(const Geo& g, std::vector<Spec>* out) {
       o.cost += 0.01;
       out->push_back(o);
     }
+    // two CTAs per SM: half the shared memory each
+    const int64_t ta = S * sp.tx * sp.ty * g.eA, tb = S * sp.tx * sp.ty * g.eB;
+    Spec h = sp;
+    h.sb = 2;
+    h.st = static_cast<int>(std::min<int64_t>(kTmaMaxStages, (110 * 1024 - 2 * tb) / ta));
+    h.cost += 0.02;
+    TmaPlan probe;
+    if (h.st >= 2 && build_tma(g, h, &probe, nullptr)) out->push_back(h);
     ++n;
   }
 }
@@ -923,6 +950,7 @@ std::string Spec::text() const {
     case kTma:
       std::snprintf(buf, sizeof buf, "kern=tma;kx=%d;ky=%d;tx=%d;ty=%d;order=%d;occ=%d;st=%d", kx, ky, tx, ty,
                     order, occ, st);
+      if (sb) std::snprintf(buf + std::strlen(buf), sizeof buf - std::strlen(buf), ";sb=%d", sb);
       break;
     default:
       std::snprintf(buf, sizeof buf,
@@ -944,7 +972,7 @@ bool Spec::parse(const std::string& s, Spec* out) {
     const auto eq = kv.find('=');
     if (eq == std::string::npos) return false;
     const std::string k = kv.substr(0, eq), v = kv.substr(eq + 1);
-    if (k == "fn") continue;  // informational (ttb_plan_describe)
+    if (k == "fn" || k == "boxes") continue;  // informational (ttb_plan_describe)
     if (k == "kern") {
       have_kern = true;
       if (v == "copy")
@@ -990,6 +1018,8 @@ bool Spec::parse(const std::string& s, Spec* out) {
       p.xp = static_cast<int>(x);
     else if (k == "ly")
       p.ly = static_cast<int>(x);
+    else if (k == "sb")
+      p.sb = static_cast<int>(x);
     else
       return false;
   }
@@ -1190,6 +1220,10 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     if (!build_space(g, xs, &c.X) || !build_space(g, ys, &c.Y) ||
         !build_space(g, outer_axes(g, xs, ys, 0), &c.O))
       return fail("copy: index space exceeds 2^31");
+    // the row length is checked in 64 bits before it narrows (a 2^32-element
+    // lead would otherwise wrap to a short or empty row)
+    if (static_cast<uint64_t>(g.n[0] / v) + 32u * 8u * 4u >= kIdxLimit)
+      return fail("copy: row length exceeds 2^31");
     c.lvec = static_cast<uint32_t>(g.n[0] / v);
     c.dl = Div32::make(c.lvec);
     c.tx = static_cast<uint32_t>(tx);
@@ -1275,6 +1309,7 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     if (!build_space(g, xs, &m.X) || !build_space(g, ys, &m.Y) ||
         !build_space(g, outer_axes(g, xs, ys, shared ? 0 : -1), &m.O))
       return fail("smem: index space exceeds 2^31");
+    if (shared && static_cast<uint64_t>(g.n[0]) >= kIdxLimit) return fail("smem: shared lead exceeds 2^31");
     m.S = shared ? static_cast<uint32_t>(g.n[0]) : 1;
     if (s.tx < 1 || s.ty < 1 || s.tx > 4096 || s.ty > 4096) return fail("smem: bad tile");
     // a shifted vector tile keeps whole vectors per side (partial tiles are masked)
@@ -1320,6 +1355,7 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
       if (s.st < 2 || s.st > 8) return fail("smem: bulk tile stages outside 2..8");
       m.dense = 5;
       m.ept = 0;
+      btile_counters_init();  // the work-stealing counters, outside any stream capture
       m.ly = 1;
       while (m.ly < 32 && m.ly < m.S * m.ty) m.ly *= 2;
       if (s.ly) {  // fewer lanes per column, more columns per warp step

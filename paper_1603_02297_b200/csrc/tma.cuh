@@ -180,13 +180,15 @@ __global__ void __launch_bounds__(32 * (NC + 2 + SW)) tma_kernel(const __grid_co
   __shared__ uint64_t fb[kTmaMaxStages], db[kTmaMaxStages], fr[kTmaMaxStages];
 
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t NS = P.ns;
+  const uint32_t NA = P.ns, NB = P.nsb;  // A ring / B ring slots
   unsigned char* ring_a = smem;
-  unsigned char* ring_b = smem + NS * P.tile_a;
+  unsigned char* ring_b = smem + NA * P.tile_a;
   if (tid == 0) {
-    for (uint32_t s = 0; s < NS; ++s) {
+    for (uint32_t s = 0; s < NA; ++s) {
       mbar_init(&fa[s], 1);
       mbar_init(&ea[s], NC);
+    }
+    for (uint32_t s = 0; s < NB; ++s) {
       mbar_init(&fb[s], 1);
       mbar_init(&db[s], NC);
       mbar_init(&fr[s], 1);
@@ -203,6 +205,7 @@ __global__ void __launch_bounds__(32 * (NC + 2 + SW)) tma_kernel(const __grid_co
     const CUtensorMap* m = is_a ? &Q.ma : &Q.mb;
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
     const uint32_t bytes = P.bx * P.by * P.S * (is_a ? eA : eB);
+    const uint32_t N = is_a ? NA : NB;
     uint32_t s = 0, ph = 0;
     for (uint32_t t = blockIdx.x; t < P.items; t += g) {
       mbar_wait(is_a ? &ea[s] : &fr[s], ph ^ 1);  // a fresh barrier passes parity 1 at once
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(32 * (NC + 2 + SW)) tma_kernel(const __grid_co
         tma_load(m, P.va.rank, ring_a + s * P.tile_a, ca, bar);
       else
         tma_load(m, P.vb.rank, ring_b + s * P.tile_b, cb, bar);
-      if (++s == NS) {
+      if (++s == N) {
         s = 0;
         ph ^= 1;
       }
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(32 * (NC + 2 + SW)) tma_kernel(const __grid_co
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&Q.mb)) : "memory");
     uint32_t k = q;
     for (uint32_t t = blockIdx.x + q * g; t < P.items; t += SW * g, k += SW) {
-      const uint32_t s = k % NS, ph = (k / NS) & 1;
+      const uint32_t s = k % NB, ph = (k / NB) & 1;
       mbar_wait(&db[s], ph);
       int ca[kTmaMaxRank], cb[kTmaMaxRank];
       tma_coords(P, t, ca, cb);
@@ -246,14 +249,14 @@ __global__ void __launch_bounds__(32 * (NC + 2 + SW)) tma_kernel(const __grid_co
   // ------------------------------------------------------------ consumers --
   const Update<SA, SB, MODE> up(P.sc);
   const uint32_t cw = warp - 2 - SW;
-  uint32_t s = 0, ph = 0;
+  uint32_t s = 0, ph = 0, sb = 0, phb = 0;
   uint32_t i = 0, j = 0;
   if (!RUNS) tma_lane<WM>(lane, P.wxl, i, j);
   for (uint32_t t = blockIdx.x; t < P.items; t += g) {
     mbar_wait(&fa[s], ph);
-    mbar_wait(UPD ? &fb[s] : &fr[s], UPD ? ph : ph ^ 1);  // beta: B landed; else: slot free
+    mbar_wait(UPD ? &fb[sb] : &fr[sb], UPD ? phb : phb ^ 1);  // beta: B landed; else: slot free
     const unsigned char* ta = ring_a + s * P.tile_a;
-    unsigned char* tb = ring_b + s * P.tile_b;
+    unsigned char* tb = ring_b + sb * P.tile_b;
     if constexpr (RUNS) {
       // (x, y) runs of S elements, K 16-byte chunks each, walked in B order
       const uint32_t total = P.bx * P.by * P.kch;
@@ -305,11 +308,15 @@ __global__ void __launch_bounds__(32 * (NC + 2 + SW)) tma_kernel(const __grid_co
     __syncwarp();
     if (lane == 0) {
       mbar_arrive(&ea[s]);
-      mbar_arrive(&db[s]);
+      mbar_arrive(&db[sb]);
     }
-    if (++s == NS) {
+    if (++s == NA) {
       s = 0;
       ph ^= 1;
+    }
+    if (++sb == NB) {
+      sb = 0;
+      phb ^= 1;
     }
   }
 }

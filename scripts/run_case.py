@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--top", type=int, default=0, help="only the first N candidates")
+    ap.add_argument("--filter", default=None, help="only candidates containing this text")
+    ap.add_argument("--extra", action="append", default=[], help="additional plan texts")
     args = ap.parse_args()
 
     import torch
@@ -39,8 +41,11 @@ def main():
     ttb.fill_uniform(w.kind, list(w.sizes), w.lda and list(w.lda), w.seed_a, a.data_ptr())
     plan = ttb.GpuPlan(p, cache=False)
     texts = [args.plan] if args.plan else plan.candidates()
+    if args.filter:
+        texts = [t for t in texts if args.filter in t]
     if args.top:
         texts = texts[:args.top]
+    texts = texts + args.extra
     golden = None
     if args.check:
         with open(os.path.join(ROOT, "tests", "golden", "config_checksums.json")) as f:
@@ -50,7 +55,11 @@ def main():
     print(f"# {w.name} kind={w.kind} merged perm={merged.perm.map} sizes={merged.sizes} "
           f"bytes={w.algorithmic_bytes}", flush=True)
     for t in texts:
-        plan.select(t)
+        try:
+            plan.select(t)
+        except Exception as e:  # a hand-written plan text that does not apply
+            print(f"   skip {t}: {e}", flush=True)
+            continue
         if w.beta != 0.0:
             ttb.fill_uniform(w.kind, w.sizes_b, w.ldb and list(w.ldb), w.seed_b, b.data_ptr())
         plan.execute(a, b)

@@ -33,6 +33,12 @@ CASES = [
     ([3, 5, 2, 6, 4, 1], [8, 5, 6, 3, 4, 4], None, None),     # rank 6 (c3-like)
     ([1, 3, 2], [8, 21, 13], None, None),                     # case 1: shared run of 8
     ([1, 4, 3, 2], [12, 5, 7, 9], [12, 6, 7, 9], [16, 9, 7, 6]),  # case 1, padded
+    # B rows (23 / 57 elements) that end inside a 16-byte chunk, padded after:
+    # a store clips them at 16-byte granularity, so no tile may be partial
+    # along them (found by the random-problem parity test)
+    ([3, 2, 1, 4], [45, 53, 23, 45], [45, 56, 23, 45], [24, 56, 45, 47]),
+    ([3, 1, 2], [56, 57, 63], [56, 57, 65], [58, 63, 56]),
+    ([2, 1], [64, 57], None, [58, 64]),
 ]
 
 

@@ -828,7 +828,13 @@ int ttb_plan_tune_cached(ttb_plan plan, const char* cache_file, const void* A, v
     const std::string pkey = cache_key(plan->orig);  // canonical_key of the original problem
     CacheEntry e;
     if (hit) *hit = 0;
-    if (cache_lookup(cache_file, pkey, hk, &e)) {
+    // a line whose plan is not a GPU plan is malformed here: it can neither
+    // be selected nor shadow an earlier entry that can
+    const auto gpu_plan = [](const std::string& t) {
+      Spec sp;
+      return Spec::parse(t, &sp);
+    };
+    if (cache_lookup(cache_file, pkey, hk, &e, gpu_plan)) {
       Spec sp;
       Prepared pr;
       if (Spec::parse(e.plan, &sp) && prepare(plan->geo, sp, plan->sms, &pr, nullptr)) {

@@ -67,16 +67,6 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 // spin on mbarrier.test_wait (non-blocking): try_wait may suspend the thread
 // for a system-dependent time after the phase completes
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#ifdef TTB_BTILE_TRYWAIT
-  asm volatile(
-      "{\n"
-      " .reg .pred done;\n"
-      "W: mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n"
-      " @!done bra W;\n"
-      "}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-#else
   asm volatile(
       "{\n"
       " .reg .pred done;\n"
@@ -85,7 +75,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
-#endif
 }
 
 // global -> shared bulk copy (TMA engine, no tensor map), completion counted
@@ -107,11 +96,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // when A's and B's stride-1 indices differ): an A tile row is then S*tx
 // elements, a B tile column S*ty.  MODE 0-3 as Update (3: B read directly
 // by the consumers, not through the ring).
-// EXP (kernel-design probes only, scripts/btile_probe.cu): bit 0 skips the B
-// stores, bit 1 skips the bulk copies (the ring still cycles), bit 2 skips the
-// consumers' work (they only wait and release)
 template <class SA, class SB, int C, int MODE, int JY, int PW = kBtileProducerWarps,
-          int NC = kBtileConsumerWarps, int EXP = 0>
+          int NC = kBtileConsumerWarps>
 __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams P) {
   using E = Vec<SA, C>;
   using EBv = Vec<SB, C>;
@@ -204,10 +190,8 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
           const uint64_t lo = ga & ~uint64_t{15};
           const uint64_t hi = (ga + static_cast<uint64_t>(end - lane) * len * esz + 15) & ~uint64_t{15};
           shift = static_cast<uint32_t>(ga - lo);
-          if constexpr (!(EXP & 2)) {
-            copy(region + i * pitch, lo, static_cast<uint32_t>(hi - lo));
-            bytes += static_cast<uint32_t>(hi - lo);
-          }
+          copy(region + i * pitch, lo, static_cast<uint32_t>(hi - lo));
+          bytes += static_cast<uint32_t>(hi - lo);
         }
         const uint32_t s0 = valid ? 31u - __clz(smask & ((2u << lane) - 1u)) : 0u;
         const uint32_t sh0 = __shfl_sync(0xffffffffu, shift, s0);
@@ -219,10 +203,8 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
         const uint64_t ga = reinterpret_cast<uint64_t>(gbase + off * esz);
         const uint64_t lo = ga & ~uint64_t{15};
         const uint64_t hi = (ga + static_cast<uint64_t>(len) * esz + 15) & ~uint64_t{15};
-        if constexpr (!(EXP & 2)) {
-          copy(region + i * pitch, lo, static_cast<uint32_t>(hi - lo));
-          bytes += static_cast<uint32_t>(hi - lo);
-        }
+        copy(region + i * pitch, lo, static_cast<uint32_t>(hi - lo));
+        bytes += static_cast<uint32_t>(hi - lo);
         tab[i] = (i * pitch + static_cast<uint32_t>(ga - lo)) / esz;
       };
       if (P.runs & 1) {
@@ -309,7 +291,7 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
       // walking X1 fastest keeps consecutive columns contiguous in B
       const bool xperm = P.xp != 0 && t.nx == P.tx;
       constexpr int U = 4;
-      for (uint32_t e0 = warp * 32 + lane; e0 < ((EXP & 4) ? 0u : total); e0 += U * 32 * NC) {
+      for (uint32_t e0 = warp * 32 + lane; e0 < total; e0 += U * 32 * NC) {
         EBv w[U];
         EBv* q[U];
         bool v[U];
@@ -352,7 +334,7 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
       const uint32_t y = P.S == 1 ? e : udiv(e, P.dS);
       rb[j] = yv[j] ? rbase[y] + (e - y * P.S) : 0u;
     }
-    for (uint32_t x0 = warp * lxn + xi; x0 < ((EXP & 4) ? 0u : t.nx); x0 += UX * xstep) {
+    for (uint32_t x0 = warp * lxn + xi; x0 < t.nx; x0 += UX * xstep) {
       EBv* q[UX];
       uint32_t xs[UX], cb[UX];
       bool xv[UX];
@@ -388,11 +370,7 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
       for (int u = 0; u < UX; ++u)
 #pragma unroll
         for (int j = 0; j < JY; ++j) {
-          if constexpr (EXP & 1) {
-            if (w[u][j].v[0] == SB(1234.5)) vstore_pred(q[u][j * ly].v, w[u][j], xv[u] && yv[j]);
-          } else {
-            vstore_pred(q[u][j * ly].v, w[u][j], xv[u] && yv[j]);
-          }
+          vstore_pred(q[u][j * ly].v, w[u][j], xv[u] && yv[j]);
         }
     }
     }

@@ -17,24 +17,23 @@ template <int NC, int PW, int... JYS>
 struct BtileCfg {
   template <class F>
   static cudaError_t with(int ka, int kb, int mode, int jy, F&& f) {
-    if (ka != kb || mode < 0 || mode > 3) return cudaErrorInvalidValue;
+    if (mode < 0 || mode > 3) return cudaErrorInvalidValue;
+    // every kind pair: A rows and B columns are fetched with their own element
+    // sizes, the epilogue converts (executor.hpp:18-31)
     return with_types(ka, kb, [&](auto t) -> cudaError_t {
       using T = decltype(t);
-      if constexpr (!std::is_same<typename T::SA, typename T::SB>::value) {
-        return cudaErrorInvalidValue;
-      } else {
-        auto modes = [&](auto&& g) -> cudaError_t {
-          if (mode == 3) return g(std::integral_constant<int, 3>{});
-          return with_mode(mode, g);
-        };
-        return modes([&](auto m) {
-          constexpr int M = decltype(m)::value;
-          using SA = typename T::SA;
-          cudaError_t r = cudaErrorInvalidValue;
-          ((jy == JYS ? (r = f(&btile_kernel<SA, SA, T::C, M, JYS, PW, NC>), true) : false) || ...);
-          return r;
-        });
-      }
+      auto modes = [&](auto&& g) -> cudaError_t {
+        if (mode == 3) return g(std::integral_constant<int, 3>{});
+        return with_mode(mode, g);
+      };
+      return modes([&](auto m) {
+        constexpr int M = decltype(m)::value;
+        using SA = typename T::SA;
+        using SB = typename T::SB;
+        cudaError_t r = cudaErrorInvalidValue;
+        ((jy == JYS ? (r = f(&btile_kernel<SA, SB, T::C, M, JYS, PW, NC>), true) : false) || ...);
+        return r;
+      });
     });
   }
 

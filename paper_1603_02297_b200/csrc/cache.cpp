@@ -1,22 +1,32 @@
-// cache.cpp -- the reference's SolutionCache file format (tuner.cpp:81-205)
-// and its benchmark-suite generator (benchmark.cpp:17-220), restated for the
-// engine's host side.
+// cache.cpp -- persistent plan store and the paper's benchmark-suite manifest.
+//
+// The store keeps the reference's on-disk contract (SolutionCache,
+// tuner.cpp:81-205) so files move between the two: one entry per line, five
+// tab-separated fields  problem_key, hardware_key, plan, GiB/s ("%.17g"),
+// ISO-8601 UTC time; a line that does not split into five non-empty fields
+// (the fifth takes the rest of the line) or whose GiB/s is not a whole
+// number is skipped and counted in one warning on stderr; the last entry for
+// a (problem, hardware) pair wins; appends take an exclusive flock, reads a
+// shared one.  A reader may also require that the plan field parses as its
+// own plan syntax (ttb_plan_tune_cached asks for a GPU plan): a line that
+// fails it counts as malformed too, so it never shadows an earlier valid one.
+//
+// The suite manifest restates build_benchmark (benchmark.cpp:166-220): the
+// same mt19937_64 draw sequence over the same lexicographic permutation
+// lists, so it reproduces the reference's manifest line for line.
 #include "cache.hpp"
 
-#include <fcntl.h>
 #include <sys/file.h>
-#include <unistd.h>
 
-#include <algorithm>
 #include <cerrno>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <ctime>
-#include <numeric>
 #include <random>
-#include <sstream>
 #include <stdexcept>
+#include <string_view>
 
 #include "problem.hpp"
 
@@ -24,239 +34,253 @@ namespace ttb {
 
 namespace {
 
-constexpr char kSep = '\t';
+// ------------------------------------------------------------- the store --
 
-bool single_line(const std::string& s) {
-  return !s.empty() && s.find_first_of("\t\n\r") == std::string::npos;
-}
-
-bool parse_line(const std::string& line, CacheEntry* e) {
-  std::vector<std::string> f;
-  size_t start = 0;
-  while (f.size() < 5) {
-    const size_t pos = line.find(kSep, start);
-    if (pos == std::string::npos) {
-      f.push_back(line.substr(start));
-      break;
+// An open solution file holding a flock for its lifetime.
+class LockedFile {
+ public:
+  LockedFile(const std::string& path, bool append) {
+    fp_ = std::fopen(path.c_str(), append ? "ae" : "re");
+    if (!fp_) {
+      if (append) throw std::runtime_error("cache: cannot open " + path);
+      return;  // no file yet: nothing stored
     }
-    f.push_back(line.substr(start, pos - start));
-    start = pos + 1;
+    if (::flock(fileno(fp_), append ? LOCK_EX : LOCK_SH) != 0) {
+      std::fclose(fp_);
+      fp_ = nullptr;
+      throw std::runtime_error("cache: lock failed");
+    }
   }
-  if (f.size() != 5) return false;
-  for (const std::string& x : f)
+  ~LockedFile() {
+    if (fp_) std::fclose(fp_);  // closing drops the lock
+  }
+  LockedFile(const LockedFile&) = delete;
+  LockedFile& operator=(const LockedFile&) = delete;
+  std::FILE* get() const { return fp_; }
+
+ private:
+  std::FILE* fp_ = nullptr;
+};
+
+// the five fields of one line: the first four end at a tab, the fifth is
+// the rest of the line; empty fields make the line malformed
+bool split_entry(std::string_view line, std::string_view (&f)[5]) {
+  for (int i = 0; i < 4; ++i) {
+    const size_t tab = line.find('\t');
+    if (tab == std::string_view::npos) return false;
+    f[i] = line.substr(0, tab);
+    line.remove_prefix(tab + 1);
+  }
+  f[4] = line;
+  for (const std::string_view& x : f)
     if (x.empty()) return false;
-  errno = 0;
-  char* end = nullptr;
-  const double bw = std::strtod(f[3].c_str(), &end);
-  if (end != f[3].c_str() + f[3].size() || errno != 0) return false;
-  e->problem_key = f[0];
-  e->hardware_key = f[1];
-  e->plan = f[2];
-  e->bandwidth_gibs = bw;
-  e->timestamp = f[4];
   return true;
 }
 
-struct Fd {
-  int fd = -1;
-  ~Fd() {
-    if (fd >= 0) ::close(fd);  // also drops the flock
-  }
-};
+bool whole_number(std::string_view text, double* out) {
+  const std::string s(text);
+  char* end = nullptr;
+  errno = 0;
+  const double v = std::strtod(s.c_str(), &end);
+  if (errno != 0 || end != s.c_str() + s.size()) return false;
+  *out = v;
+  return true;
+}
+
+bool one_line(const std::string& s) { return !s.empty() && s.find_first_of("\t\r\n") == std::string::npos; }
 
 }  // namespace
 
-bool cache_lookup(const std::string& file, const std::string& problem_key,
-                  const std::string& hardware_key, CacheEntry* out) {
-  Fd f;
-  f.fd = ::open(file.c_str(), O_RDONLY | O_CLOEXEC);
-  if (f.fd < 0) return false;
-  if (::flock(f.fd, LOCK_SH) != 0) throw std::runtime_error("cache: lock failed");
-  std::string text;
-  char buf[1 << 16];
-  ssize_t got;
-  while ((got = ::read(f.fd, buf, sizeof buf)) > 0) text.append(buf, static_cast<size_t>(got));
-  if (got < 0) throw std::runtime_error("cache: read failed");
+bool cache_lookup(const std::string& file, const std::string& problem_key, const std::string& hardware_key,
+                  CacheEntry* out, const std::function<bool(const std::string&)>& plan_ok) {
+  LockedFile lf(file, false);
+  if (!lf.get()) return false;
   bool found = false;
-  int bad = 0;
-  size_t start = 0;
-  while (start < text.size()) {
-    size_t nl = text.find('\n', start);
-    if (nl == std::string::npos) nl = text.size();
-    const std::string line = text.substr(start, nl - start);
-    start = nl + 1;
+  int skipped = 0;
+  char* buf = nullptr;
+  size_t cap = 0;
+  ssize_t n;
+  while ((n = ::getline(&buf, &cap, lf.get())) >= 0) {
+    std::string_view line(buf, static_cast<size_t>(n));
+    if (!line.empty() && line.back() == '\n') line.remove_suffix(1);
     if (line.empty()) continue;
-    CacheEntry e;
-    if (!parse_line(line, &e)) {
-      ++bad;
+    std::string_view f[5];
+    double gibs = 0.0;
+    if (!split_entry(line, f) || !whole_number(f[3], &gibs) || (plan_ok && !plan_ok(std::string(f[2])))) {
+      ++skipped;
       continue;
     }
-    if (e.problem_key == problem_key && e.hardware_key == hardware_key) {
-      *out = e;
-      found = true;
-    }
+    if (f[0] != problem_key || f[1] != hardware_key) continue;
+    *out = CacheEntry{std::string(f[0]), std::string(f[1]), std::string(f[2]), gibs, std::string(f[4])};
+    found = true;
   }
-  if (bad > 0)
-    std::fprintf(stderr, "warning: cache %s: skipped %d malformed line(s)\n", file.c_str(), bad);
+  const bool read_error = std::ferror(lf.get()) != 0;
+  std::free(buf);
+  if (read_error) throw std::runtime_error("cache: read failed");
+  if (skipped) std::fprintf(stderr, "warning: cache %s: skipped %d malformed line(s)\n", file.c_str(), skipped);
   return found;
 }
 
 void cache_store(const std::string& file, const CacheEntry& e) {
-  if (!single_line(e.problem_key) || !single_line(e.hardware_key) || !single_line(e.plan) ||
-      !single_line(e.timestamp))
+  if (!one_line(e.problem_key) || !one_line(e.hardware_key) || !one_line(e.plan) || !one_line(e.timestamp))
     throw InvalidArgument{"cache: entry fields must be non-empty single-line text"};
-  char bw[64];
-  std::snprintf(bw, sizeof bw, "%.17g", e.bandwidth_gibs);
-  const std::string line = e.problem_key + kSep + e.hardware_key + kSep + e.plan + kSep + bw +
-                           kSep + e.timestamp + '\n';
-  Fd f;
-  f.fd = ::open(file.c_str(), O_WRONLY | O_CREAT | O_APPEND | O_CLOEXEC, 0644);
-  if (f.fd < 0) throw std::runtime_error("cache: cannot open " + file);
-  if (::flock(f.fd, LOCK_EX) != 0) throw std::runtime_error("cache: lock failed");
-  size_t off = 0;
-  while (off < line.size()) {
-    const ssize_t put = ::write(f.fd, line.data() + off, line.size() - off);
-    if (put < 0) throw std::runtime_error("cache: write failed");
-    off += static_cast<size_t>(put);
-  }
+  char gibs[64];
+  std::snprintf(gibs, sizeof gibs, "%.17g", e.bandwidth_gibs);
+  const std::string line =
+      e.problem_key + '\t' + e.hardware_key + '\t' + e.plan + '\t' + gibs + '\t' + e.timestamp + '\n';
+  LockedFile lf(file, true);
+  // one write of the whole line under the exclusive lock (O_APPEND)
+  if (std::fwrite(line.data(), 1, line.size(), lf.get()) != line.size() || std::fflush(lf.get()) != 0)
+    throw std::runtime_error("cache: write failed");
 }
 
 std::string iso8601_utc_now() {
-  const std::time_t now = std::time(nullptr);
-  std::tm tm{};
-  gmtime_r(&now, &tm);
+  const std::time_t t = std::chrono::system_clock::to_time_t(std::chrono::system_clock::now());
+  std::tm u{};
+  gmtime_r(&t, &u);
   char buf[32];
-  std::strftime(buf, sizeof buf, "%Y-%m-%dT%H:%M:%SZ", &tm);
+  std::snprintf(buf, sizeof buf, "%04d-%02d-%02dT%02d:%02d:%02dZ", u.tm_year + 1900, u.tm_mon + 1, u.tm_mday,
+                u.tm_hour, u.tm_min, u.tm_sec);
   return buf;
 }
 
-// --------------------------------------------------------------- suite --
+// ------------------------------------------------------------- the suite --
 
 namespace {
 
-// uniform draw in [0, n) by rejection (benchmark.cpp:19-24)
-uint64_t below(std::mt19937_64& g, uint64_t n) {
-  const uint64_t lim = UINT64_MAX - UINT64_MAX % n;
-  uint64_t v = g();
-  while (v >= lim) v = g();
-  return v % n;
-}
-
-std::vector<int> reversed(int d) {
-  std::vector<int> p(static_cast<size_t>(d));
-  for (int i = 0; i < d; ++i) p[static_cast<size_t>(i)] = d - i;
-  return p;
-}
-
-// perms (1-based maps, lexicographic order) with no adjacent +1 pair, i.e.
-// nothing merge_indices could fuse; stride-1 keepers start with 1 and are not
-// the identity, the general ones move index 1 and are not the reversal
-std::vector<std::vector<int>> candidates_of(int d, bool keep_stride1) {
-  std::vector<int> p(static_cast<size_t>(d));
-  std::iota(p.begin(), p.end(), 1);
-  const std::vector<int> rev = reversed(d);
-  std::vector<std::vector<int>> out;
-  do {
-    bool fusable = false;
-    for (size_t a = 0; a + 1 < p.size(); ++a) fusable = fusable || p[a + 1] == p[a] + 1;
-    if (fusable) continue;
-    if (keep_stride1) {
-      bool ident = true;
-      for (size_t i = 0; i < p.size(); ++i) ident = ident && p[i] == static_cast<int>(i) + 1;
-      if (p[0] == 1 && !ident) out.push_back(p);
-    } else if (p[0] != 1 && p != rev) {
-      out.push_back(p);
+// unbiased draw in [0, n): reject the top partial block of the 64-bit range
+struct SuiteDraws {
+  std::mt19937_64 eng;
+  explicit SuiteDraws(uint64_t seed) : eng(seed) {}
+  uint64_t below(uint64_t n) {
+    const uint64_t cut = UINT64_MAX - UINT64_MAX % n;
+    for (;;) {
+      const uint64_t v = eng();
+      if (v < cut) return v % n;
     }
-  } while (std::next_permutation(p.begin(), p.end()));
+  }
+};
+
+// 1-based maps of rank d in lexicographic order, without an adjacent pair
+// (m, m+1) -- nothing index merging could fuse -- pruned while building
+void unmergeable_maps(int d, std::vector<int>* cur, std::vector<bool>* used, std::vector<std::vector<int>>* out) {
+  if (static_cast<int>(cur->size()) == d) {
+    out->push_back(*cur);
+    return;
+  }
+  for (int v = 1; v <= d; ++v) {
+    if ((*used)[static_cast<size_t>(v)] || (!cur->empty() && cur->back() + 1 == v)) continue;
+    (*used)[static_cast<size_t>(v)] = true;
+    cur->push_back(v);
+    unmergeable_maps(d, cur, used, out);
+    cur->pop_back();
+    (*used)[static_cast<size_t>(v)] = false;
+  }
+}
+
+std::vector<int> descending(int d) {
+  std::vector<int> m;
+  for (int v = d; v >= 1; --v) m.push_back(v);
+  return m;
+}
+
+// stride-1 keepers: map[0] == 1 (and not the identity, which is mergeable
+// anyway); general: map[0] != 1 and not the full reversal
+std::vector<std::vector<int>> suite_maps(int d, bool keeps_stride1) {
+  std::vector<std::vector<int>> all, out;
+  std::vector<int> cur;
+  std::vector<bool> used(static_cast<size_t>(d) + 1, false);
+  unmergeable_maps(d, &cur, &used, &all);
+  const std::vector<int> rev = descending(d);
+  for (const std::vector<int>& m : all) {
+    const bool first = m[0] == 1;
+    if (keeps_stride1 ? first : (!first && m != rev)) out.push_back(m);
+  }
   return out;
 }
 
-double deviation(const std::vector<int64_t>& s, int64_t target) {
-  int64_t n = 1;
-  for (int64_t e : s) n *= e;
-  return std::fabs(static_cast<double>(n) / static_cast<double>(target) - 1.0);
+double off_target(const std::vector<int64_t>& ext, int64_t target) {
+  int64_t p = 1;
+  for (int64_t e : ext) p *= e;
+  return std::fabs(static_cast<double>(p) / static_cast<double>(target) - 1.0);
 }
 
-// extents near the d-th root of the element count; `skew` (>= 0) is 6x the
-// others; one axis absorbs the rounding (benchmark.cpp:73-99)
-std::vector<int64_t> shape(int d, int64_t target, int skew) {
-  const double scale = skew < 0 ? 1.0 : 6.0;
-  const double root = std::pow(static_cast<double>(target) / scale, 1.0 / d);
-  std::vector<int64_t> best;
-  double best_dev = 1e300;
-  for (int bump = 0; bump < 2; ++bump) {
-    const int64_t s = std::max<int64_t>(2, static_cast<int64_t>(root) + bump);
-    std::vector<int64_t> v(static_cast<size_t>(d), s);
-    int adj = d - 1;
-    if (skew >= 0) {
-      v[static_cast<size_t>(skew)] = 6 * s;
-      if (adj == skew) adj = d - 2;
-    }
-    int64_t rest = 1;
+// d extents of about target^(1/d) (the skew axis, if any, 6x its share);
+// the last axis (the one before it when that is the skew axis) absorbs the
+// rounding; of the floor root and the root + 1 the closer volume wins
+std::vector<int64_t> suite_extents(int d, int64_t target, int skew) {
+  const double side = std::pow(static_cast<double>(target) / (skew < 0 ? 1.0 : 6.0), 1.0 / d);
+  const int fix = (skew == d - 1) ? d - 2 : d - 1;
+  std::vector<int64_t> pick;
+  double err = 1e300;
+  for (int64_t s : {static_cast<int64_t>(side), static_cast<int64_t>(side) + 1}) {
+    s = std::max<int64_t>(2, s);
+    std::vector<int64_t> ext(static_cast<size_t>(d), s);
+    if (skew >= 0) ext[static_cast<size_t>(skew)] = 6 * s;
+    int64_t others = 1;
     for (int i = 0; i < d; ++i)
-      if (i != adj) rest *= v[static_cast<size_t>(i)];
-    v[static_cast<size_t>(adj)] = std::max<int64_t>(
-        2, static_cast<int64_t>(std::llround(static_cast<double>(target) / static_cast<double>(rest))));
-    const double dev = deviation(v, target);
-    if (dev < best_dev) {
-      best_dev = dev;
-      best = v;
+      if (i != fix) others *= ext[static_cast<size_t>(i)];
+    ext[static_cast<size_t>(fix)] = std::max<int64_t>(
+        2, static_cast<int64_t>(std::llround(static_cast<double>(target) / static_cast<double>(others))));
+    const double e = off_target(ext, target);
+    if (e < err) {
+      err = e;
+      pick = ext;
     }
   }
-  return best;
+  return pick;
 }
 
 template <class T>
-std::string joined(const std::vector<T>& v, char sep) {
-  std::ostringstream os;
-  for (size_t i = 0; i < v.size(); ++i) os << (i ? std::string(1, sep) : "") << v[i];
-  return os.str();
+std::string comma_list(const std::vector<T>& v) {
+  std::string s;
+  for (const T& x : v) s += (s.empty() ? "" : ",") + std::to_string(x);
+  return s;
 }
 
 }  // namespace
 
 std::vector<std::string> benchmark_manifest(int64_t volume_bytes, int kind, uint64_t seed) {
-  if (volume_bytes < (1 << 20)) throw InvalidArgument{"benchmark: volume must be at least 1 MiB"};
+  if (volume_bytes < (int64_t{1} << 20)) throw InvalidArgument{"benchmark: volume must be at least 1 MiB"};
   if (kind < 0 || kind > 3) throw InvalidArgument{"benchmark: bad element kind"};
   const int64_t target = volume_bytes / kind_bytes(kind);
-  std::mt19937_64 g(seed);
-  std::vector<std::pair<std::vector<int>, const char*>> perms;
-  perms.emplace_back(reversed(2), "inverse");
+  SuiteDraws draws(seed);
+  struct Pick {
+    std::vector<int> map;
+    const char* category;
+  };
+  std::vector<Pick> picks{{descending(2), "inverse"}};
   for (int d = 3; d <= 6; ++d) {
-    perms.emplace_back(reversed(d), "inverse");
-    const auto keep = candidates_of(d, true);
-    perms.emplace_back(keep[below(g, keep.size())], "stride1");
-    const auto gen = candidates_of(d, false);
-    const int want = d == 3 ? 1 : 3;
-    std::vector<std::vector<int>> chosen;
-    while (static_cast<int>(chosen.size()) < want) {
-      const auto& pick = gen[below(g, gen.size())];
-      if (std::find(chosen.begin(), chosen.end(), pick) == chosen.end()) chosen.push_back(pick);
+    picks.push_back({descending(d), "inverse"});
+    const std::vector<std::vector<int>> keep = suite_maps(d, true);
+    picks.push_back({keep[draws.below(keep.size())], "stride1"});
+    const std::vector<std::vector<int>> gen = suite_maps(d, false);
+    std::vector<std::vector<int>> mine;
+    while (static_cast<int>(mine.size()) < (d == 3 ? 1 : 3)) {
+      const std::vector<int>& m = gen[draws.below(gen.size())];
+      bool seen = false;
+      for (const auto& q : mine) seen = seen || q == m;
+      if (!seen) mine.push_back(m);
     }
-    for (auto& c : chosen) perms.emplace_back(c, "general");
+    for (const auto& m : mine) picks.push_back({m, "general"});
   }
-  std::vector<std::string> lines;
-  const char kc = kind_letter(kind);
-  for (const auto& [perm, category] : perms) {
-    const int d = static_cast<int>(perm.size());
-    int inv0 = 0;  // the A index that lands on B's first position
-    for (int a = 0; a < d; ++a)
-      if (perm[static_cast<size_t>(a)] == 1) inv0 = a;
-    const std::pair<const char*, int> configs[] = {{"balanced", -1}, {"skewA", 0}, {"skewB", inv0}};
-    for (const auto& [cname, skew] : configs) {
-      const std::vector<int64_t> sizes = shape(d, target, skew);
-      if (deviation(sizes, target) > 0.10)
-        throw std::runtime_error("benchmark: volume too small for a ratio-6 shape at dimension " +
-                                 std::to_string(d));
+  std::vector<std::string> out;
+  const std::string kinds(2, kind_letter(kind));
+  for (const Pick& pk : picks) {
+    const int d = static_cast<int>(pk.map.size());
+    int b0 = 0;  // the A axis at B's first position (skewB widens it)
+    while (pk.map[static_cast<size_t>(b0)] != 1) ++b0;
+    for (const auto& [name, skew] : {std::pair<const char*, int>{"balanced", -1}, {"skewA", 0}, {"skewB", b0}}) {
+      const std::vector<int64_t> ext = suite_extents(d, target, skew);
+      if (off_target(ext, target) > 0.10)
+        throw std::runtime_error("benchmark: volume too small for a ratio-6 shape at dimension " + std::to_string(d));
       std::string id = "d" + std::to_string(d) + "_";
-      for (int v : perm) id += std::to_string(v);
-      id += std::string("_") + cname;
-      lines.push_back("case=" + id + ";perm=" + joined(perm, ',') + ";size=" + joined(sizes, ',') +
-                      ";kinds=" + std::string(2, kc) + ";alpha=1;beta=1;category=" + category +
-                      ";config=" + cname);
+      for (int v : pk.map) id += std::to_string(v);
+      out.push_back("case=" + id + "_" + name + ";perm=" + comma_list(pk.map) + ";size=" + comma_list(ext) +
+                    ";kinds=" + kinds + ";alpha=1;beta=1;category=" + pk.category + ";config=" + name);
     }
   }
-  return lines;
+  return out;
 }
 
 }  // namespace ttb

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -15,9 +16,11 @@ struct CacheEntry {
   std::string timestamp;
 };
 
-// last entry matching both keys; false when none (or no file)
+// last well-formed entry matching both keys; false when none (or no file).
+// plan_ok, if given, must accept the plan field or the line is malformed.
 bool cache_lookup(const std::string& file, const std::string& problem_key,
-                  const std::string& hardware_key, CacheEntry* out);
+                  const std::string& hardware_key, CacheEntry* out,
+                  const std::function<bool(const std::string&)>& plan_ok = nullptr);
 // append under an exclusive lock; InvalidArgument for empty / multi-line fields
 void cache_store(const std::string& file, const CacheEntry& e);
 std::string iso8601_utc_now();

@@ -40,12 +40,9 @@ __host__ __device__ inline uint32_t dense_stage_bytes(uint32_t tx, uint32_t ty, 
   return tables + tile_a + tile_b;
 }
 
-#ifndef TTB_DENSE_MINB
-#define TTB_DENSE_MINB 1
-#endif
 template <class SA, class SB, int C, int MODE, int EPT, int NS>
 __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == sizeof(SB))
-                                           ? TTB_DENSE_MINB
+                                           ? 1
                                            : 4) dense_kernel(const SmemParams P) {
   static_assert(EPT > 0 && NS >= 2, "dense tile");
   using E = Vec<SA, C>;
@@ -100,9 +97,7 @@ __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == size
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
       const uint32_t y = yl + k * R;  // < ty: the table read is in bounds even when masked
-#ifndef TTB_EXP_NOLOAD  // experiment switch: time the store side alone
       cp_async_pred<EB>(dst + k * R * P.rl, ax + ra[y], xv && y < t.ny);
-#endif
     }
     if constexpr (MODE == 2) {  // the tile's B elements, in the store walk's layout
       const uint32_t* cb = colB(s);
@@ -168,11 +163,7 @@ __global__ void __launch_bounds__(256, (MODE < 2 && C == 1 && sizeof(SA) == size
       for (int u = 0; u < U; ++u) {
 #pragma unroll
         for (int c = 0; c < C; ++c) w[u].v[c] = up(a[u].v[c], w[u].v[c]);
-#ifndef TTB_EXP_NOSTORE  // experiment switch: time the load side alone
         vstore_pred(q[u]->v, w[u], v[u]);
-#else
-        if (a[u].v[0] == SA(12345.678)) vstore_pred(q[u]->v, w[u], v[u]);  // keep the reads live
-#endif
       }
     }
     __syncthreads();

@@ -1,6 +1,5 @@
 // kern_btile.cu -- instantiation and launch of btile_kernel (btile.cuh) with
-// the default warp roles: the four same-kind pairs (mixed pairs run on the
-// other staged tiles), update modes 0-3 (3: beta != 0 with B read directly,
+// the default warp roles: the eight kind pairs, update modes 0-3 (3: beta != 0 with B read directly,
 // not through the ring), 1-16 column elements per consumer lane or the linear
 // walk (0).  Tiles of 32 KB and more run with twice the warps
 // (kern_btile_big.cu), selected by the launch's block size.

@@ -227,15 +227,12 @@ __device__ __forceinline__ bool copy_row(const CopyParams& P, uint32_t r, int64_
 // 32 * lvec vectors of those rows with consecutive lanes on consecutive
 // vectors, fetching each vector's row offsets by warp shuffle -- no per-vector
 // index decode.  U vectors per lane in flight.
-#ifndef TTB_COPY_U
-#define TTB_COPY_U 4
-#endif
 template <class SA, class SB, int C, int V, int MODE>
 __global__ void __launch_bounds__(256) copy_kernel(const CopyParams P) {
   const Update<SA, SB, MODE> up(P.sc);
   const SA* __restrict__ A = static_cast<const SA*>(P.A);
   SB* __restrict__ B = static_cast<SB*>(P.B);
-  constexpr int U = TTB_COPY_U;
+  constexpr int U = 4;  // vectors per lane in flight
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < P.items; it += nwarps) {

@@ -286,7 +286,7 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
       std::vector<int64_t> txs, tys;
       sides(NX, &txs);
       sides(NY, &tys);
-      if (fast && g.ka == g.kb && x_dense_in_a(g, xs, S) && y_dense_in_b(g, ys, S)) {
+      if (fast && x_dense_in_a(g, xs, S) && y_dense_in_b(g, ys, S)) {
         // bulk-copy tiles (btile.cuh): A rows of S*tx and B columns of S*ty
         // elements (S*ty <= 512), 8-64 KB of tile, 2-3 ring stages
         auto bsides = [](int64_t N, int64_t cap) {
@@ -1347,8 +1347,8 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     if (s.vec == 3 || s.vec == 4) {
       // bulk-copy tile (btile.cuh): one cp.async.bulk per A row (and B column
       // when beta != 0), any element alignment, warp-specialised ring
-      if (!(small && g.ka == g.kb && x_dense_in_a(g, xs, m.S) && y_dense_in_b(g, ys, m.S)))
-        return fail("smem: bulk tile needs equal kinds, contiguous X in A and Y in B");
+      if (!(small && x_dense_in_a(g, xs, m.S) && y_dense_in_b(g, ys, m.S)))
+        return fail("smem: bulk tile needs contiguous X in A and Y in B");
       const bool lin = s.vec == 4;  // linear walk (any column length)
       if (m.tx > 1024 || m.ty > 1024 || (!lin && (m.tx > 256 || m.ty > 256 || m.S * m.ty > 512)))
         return fail("smem: bulk tile too large");

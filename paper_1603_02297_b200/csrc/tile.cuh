@@ -65,11 +65,8 @@ __device__ __forceinline__ TileBox tile_box(const SmemParams& P, uint32_t it) {
 // KK > 0: both walks have exactly KK steps covering the tile (S*tx and S*ty
 // divide 256 and tx*ty*S = 256*KK), so the loops unroll completely and need
 // neither a step bound nor a table clamp.  KK == 0: any shape.
-#ifndef TTB_TILE_MINB
-#define TTB_TILE_MINB 1
-#endif
 template <class SA, class SB, int C, int MODE, int KK>
-__global__ void __launch_bounds__(256, KK > 0 ? TTB_TILE_MINB : 1) tile_kernel(const SmemParams P) {
+__global__ void __launch_bounds__(256, 1) tile_kernel(const SmemParams P) {
   using EA = Vec<SA, C>;
   using EBv = Vec<SB, C>;
   constexpr int EAB = static_cast<int>(sizeof(EA));

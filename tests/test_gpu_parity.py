@@ -379,12 +379,22 @@ def test_tune_cached_miss_then_hit(tmp_path, coracle):
         assert e is not None and e.plan.startswith("kern=") and e.bandwidth_gibs > 0
         assert plan.describe().startswith(e.plan)
     assert len(f.read_text().splitlines()) == 1
+    # a later line whose plan is not a GPU plan is malformed for this reader:
+    # it does not shadow the valid entry (still a hit, nothing appended)
     ttb.SolutionCache(f).store(ttb.SolutionEntry(ttb.canonical_key(p), hw, "kern=bogus", 1.0))
+    dA, dB = _dev(A), _dev(B)
+    assert ttb.GpuPlan(p, cache=False).tune_cached(dA, dB, f) is True
+    torch.cuda.synchronize()
+    assert dB.cpu().numpy().tobytes() == want.tobytes()
+    assert len(f.read_text().splitlines()) == 2
+    # a GPU plan that parses but does not apply to the problem is stale: re-tune, append
+    ttb.SolutionCache(f).store(ttb.SolutionEntry(ttb.canonical_key(p), hw,
+                                                 "kern=copy;v=4;kx=0;ky=0;tx=1;ty=1;order=0;occ=0", 1.0))
     dA, dB = _dev(A), _dev(B)
     assert ttb.GpuPlan(p, cache=False).tune_cached(dA, dB, f) is False
     torch.cuda.synchronize()
     assert dB.cpu().numpy().tobytes() == want.tobytes()
-    assert len(f.read_text().splitlines()) == 3
+    assert len(f.read_text().splitlines()) == 4
 
 
 def test_large_rank1_copy_every_copy_variant():
@@ -415,16 +425,22 @@ def test_large_rank1_copy_every_copy_variant():
     ("c", [3, 2, 1], [4, 300, 260], 1.0, 0.0),      # c4-like, complex64
     ("s", [1, 3, 2], [49, 300, 70], 1.0, 0.5),      # c5_t10-like: shared lead S = 49
     ("s", [5, 2, 4, 1, 3], [10, 64, 6, 36, 5], 1.0, 0.5),  # c5_t18-like: column-permuted walk (xp)
+    ("sd", [2, 1], [1000, 700], 1.3, 0.0),          # mixed kinds on the bulk tiles (s -> d)
+    ("ds", [3, 1, 2], [75, 40, 130], 0.7, 1.1),     # d -> s with the B ring
+    ("cz", [3, 2, 1], [5, 300, 130], 1.0, 0.5),     # c -> z, X group of two axes
+    ("zc", [2, 1], [300, 170], 2.0, 0.0),
 ])
 def test_medium_problems_every_variant(coracle, ka, perm, sizes, alpha, beta):
     """Tiles of 32-64 KB only exist on problems of a few hundred per side: every
-    candidate of these (incl. the big bulk tiles) bit-exact against the oracle."""
+    candidate of these (incl. the big bulk tiles, and the mixed kind pairs on
+    them) bit-exact against the oracle."""
+    ka, kb = (ka[0], ka[1]) if len(ka) == 2 else (ka, ka)
     rng = np.random.default_rng(sum(sizes))
-    A, B = _inputs(coracle, rng, ka, ka, perm, sizes, None, None, beta)
+    A, B = _inputs(coracle, rng, ka, kb, perm, sizes, None, None, beta)
     want = B.copy()
-    coracle.transpose(ka, ka, perm, sizes, None, None, alpha, A, beta, want)
-    texts = all_plans(ka, ka, perm, sizes, None, None, alpha, beta)
+    coracle.transpose(ka, kb, perm, sizes, None, None, alpha, A, beta, want)
+    texts = all_plans(ka, kb, perm, sizes, None, None, alpha, beta)
     assert any("vec=3" in t or "vec=4" in t for t in texts)
     for text in texts:
-        got = run_gpu(ka, ka, perm, sizes, None, None, alpha, A, beta, B, plan_text=text)
+        got = run_gpu(ka, kb, perm, sizes, None, None, alpha, A, beta, B, plan_text=text)
         assert got.tobytes() == want.tobytes(), text

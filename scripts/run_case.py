@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--top", type=int, default=0, help="only the first N candidates")
     ap.add_argument("--filter", default=None, help="only candidates containing this text")
     ap.add_argument("--extra", action="append", default=[], help="additional plan texts")
+    ap.add_argument("--kinds", default=None, help="override the kind pair, e.g. sd or cz")
     args = ap.parse_args()
 
     import torch
@@ -33,12 +34,15 @@ def main():
     from paper_1603_02297_b200.workloads import BY_NAME
 
     w = BY_NAME[args.case]
-    p = ttb.make_problem(w.perm, list(w.sizes), w.kind, w.kind, w.alpha, w.beta,
+    ka, kb = (args.kinds[0], args.kinds[1]) if args.kinds else (w.kind, w.kind)
+    from paper_1603_02297_b200.workloads import KIND_BYTES
+    nbytes = w.elements * (KIND_BYTES[ka] + KIND_BYTES[kb] * (2 if w.beta != 0.0 else 1))
+    p = ttb.make_problem(w.perm, list(w.sizes), ka, kb, w.alpha, w.beta,
                          w.lda and list(w.lda), w.ldb and list(w.ldb))
     na, nb = ttb.required_elements_a(p), ttb.required_elements_b(p)
-    a, b = ttb.TensorBuffer(w.kind, na), ttb.TensorBuffer(w.kind, nb)
-    ttb.fill_sentinel(w.kind, na, a.data_ptr())
-    ttb.fill_uniform(w.kind, list(w.sizes), w.lda and list(w.lda), w.seed_a, a.data_ptr())
+    a, b = ttb.TensorBuffer(ka, na), ttb.TensorBuffer(kb, nb)
+    ttb.fill_sentinel(ka, na, a.data_ptr())
+    ttb.fill_uniform(ka, list(w.sizes), w.lda and list(w.lda), w.seed_a, a.data_ptr())
     plan = ttb.GpuPlan(p, cache=False)
     texts = [args.plan] if args.plan else plan.candidates()
     if args.filter:
@@ -53,7 +57,7 @@ def main():
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     merged = ttb.merge_indices(p).problem
     print(f"# {w.name} kind={w.kind} merged perm={merged.perm.map} sizes={merged.sizes} "
-          f"bytes={w.algorithmic_bytes}", flush=True)
+          f"bytes={nbytes} kinds={ka}{kb}", flush=True)
     for t in texts:
         try:
             plan.select(t)
@@ -61,10 +65,10 @@ def main():
             print(f"   skip {t}: {e}", flush=True)
             continue
         if w.beta != 0.0:
-            ttb.fill_uniform(w.kind, w.sizes_b, w.ldb and list(w.ldb), w.seed_b, b.data_ptr())
+            ttb.fill_uniform(kb, w.sizes_b, w.ldb and list(w.ldb), w.seed_b, b.data_ptr())
         plan.execute(a, b)
         ok = ""
-        if golden is not None:
+        if golden is not None and not args.kinds:
             ck = ttb.checksum(w.kind, w.sizes_b, w.ldb and list(w.ldb), b.data_ptr())
             ok = " ok" if ck == golden else " MISMATCH"
         best = 1e30
@@ -74,7 +78,7 @@ def main():
             e1.record()
             e1.synchronize()
             best = min(best, e0.elapsed_time(e1))
-        print(f"{best * 1e3:9.1f} us {w.algorithmic_bytes / 1e9 / (best / 1e3):8.1f} GB/s  {t}{ok}",
+        print(f"{best * 1e3:9.1f} us {nbytes / 1e9 / (best / 1e3):8.1f} GB/s  {t}{ok}",
               flush=True)
 
 

@@ -170,6 +170,19 @@ int ttb_plan_select(ttb_plan plan, const char* plan_text);
    boxes an oversized problem runs as */
 int ttb_plan_launches(ttb_plan plan, int* launches_per_execute);
 
+/* Standalone CUDA source for one plan on one problem (replaces ttune's
+ * emit_source, emit.cpp:622-715, which writes C/OpenMP): the header and .cu
+ * text of a kernel whose extents, strides and tile are compile-time
+ * constants, entry `transpose_<perm>_<sizes>_<kinds>(const TA* A, TB* B,
+ * TW alpha, TW beta)` (device pointers, default stream) plus `<entry>_async`
+ * with a stream.  plan_text: a serialized plan (ttb_plan_describe) or NULL;
+ * basename: file stem the source includes its header by (NULL: the entry
+ * symbol).  Any output buffer may be NULL; no device is needed. */
+int ttb_emit_source(int kind_a, int kind_b, int rank, const int* perm, const int64_t* sizes,
+                    const int64_t* lda, const int64_t* ldb, double alpha, double beta,
+                    const char* plan_text, const char* basename, char* entry, size_t entry_len,
+                    char* header, size_t header_len, char* source, size_t source_len);
+
 /* ------------------------------------------ persistent solution cache -- */
 
 /* The reference's SolutionCache (tuner.cpp:81-205) as a native file store:

@@ -30,7 +30,7 @@ __all__ = [
     "reference_transpose", "execute_plan", "GpuPlan", "bandwidth_gbs", "shard_boxes",
     "fill_uniform", "fill_sentinel", "checksum", "launch_count", "TTBError", "version",
     "SolutionEntry", "SolutionCache", "hardware_key", "BenchmarkCase", "build_benchmark",
-    "benchmark_case_line",
+    "benchmark_case_line", "EmittedKernel", "emit_source", "write_kernel_files",
 ]
 
 
@@ -494,6 +494,49 @@ class GpuPlan:
         n = C.c_int(0)
         check(lib.ttb_plan_launches(self._h, C.byref(n)))
         return n.value
+
+
+class EmittedKernel:
+    """emit.hpp:27-34: entry symbol, header / source text and file names."""
+
+    def __init__(self, entry_symbol: str, include_name: str, header_text: str, source_text: str):
+        self.entry_symbol = entry_symbol
+        self.include_name = include_name
+        self.header_text = header_text
+        self.source_text = source_text
+        self.source_extension = "cu"
+        self.header_extension = "h"
+
+
+def emit_source(p: TransposeProblem, plan=None, basename: str = "") -> EmittedKernel:
+    """Standalone sm_100a CUDA source for `plan` (a GpuPlan, a plan text or None)
+    on `p` (emit.cpp:622-715 analogue; no device needed)."""
+    validate(p)
+    text = plan.describe() if isinstance(plan, GpuPlan) else plan
+    ent = C.create_string_buffer(1024)
+    hdr = C.create_string_buffer(1 << 14)
+    src = C.create_string_buffer(1 << 17)
+    check(lib.ttb_emit_source(*p._args(), p.alpha, p.beta, text.encode() if text else None,
+                              basename.encode() if basename else None, ent, 1024, hdr, 1 << 14,
+                              src, 1 << 17))
+    entry = ent.value.decode()
+    return EmittedKernel(entry, f"{basename or entry}.h", hdr.value.decode(), src.value.decode())
+
+
+def write_kernel_files(kernel: EmittedKernel, base) -> Tuple[str, str]:
+    """emit.cpp write_kernel_files: <base>.cu and the header next to it."""
+    import os  # noqa: PLC0415
+    base = str(base)
+    d = os.path.dirname(base)
+    if d:
+        os.makedirs(d, exist_ok=True)
+    src = base + "." + kernel.source_extension
+    hdr = os.path.join(d, kernel.include_name)
+    with open(src, "w") as f:
+        f.write(kernel.source_text)
+    with open(hdr, "w") as f:
+        f.write(kernel.header_text)
+    return src, hdr
 
 
 def execute_plan(p: TransposeProblem, plan: Optional[GpuPlan], a: TensorBuffer, b: TensorBuffer,

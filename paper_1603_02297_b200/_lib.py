@@ -47,6 +47,9 @@ _SIGS = {
     "ttb_plan_candidates": ([vp, C.c_char_p, C.c_size_t], C.c_int),
     "ttb_plan_select": ([vp, C.c_char_p], C.c_int),
     "ttb_plan_launches": ([vp, i32p], C.c_int),
+    "ttb_emit_source": ([C.c_int, C.c_int, C.c_int, i32p, i64p, i64p, i64p, C.c_double, C.c_double,
+                         C.c_char_p, C.c_char_p, C.c_char_p, C.c_size_t, C.c_char_p, C.c_size_t,
+                         C.c_char_p, C.c_size_t], C.c_int),
     "ttb_shard_boxes": ([C.c_int, i32p, i64p, C.c_int, C.c_int, i64p, i64p, i32p], C.c_int),
     "ttb_fill_uniform": ([C.c_int, C.c_int, i64p, i64p, i64p, i64p, C.c_uint64, vp, vp], C.c_int),
     "ttb_fill_sentinel": ([C.c_int, C.c_int64, vp, vp], C.c_int),

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cctype>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -25,6 +26,10 @@
 
 namespace ttb {
 unsigned long long launch_total();
+std::string emit_entry_symbol(const Problem& p);
+void emit_cuda(const Problem& m, const Geo& g, const Spec& spec, const std::string& base,
+               const std::string& plan_text, const std::string& key, std::string* header,
+               std::string* source);
 }
 
 using namespace ttb;
@@ -916,6 +921,38 @@ int ttb_plan_launches(ttb_plan plan, int* launches_per_execute) {
   // one kernel per execute, one per box for oversized problems
   if (launches_per_execute) *launches_per_execute = plan->boxes.empty() ? 1 : static_cast<int>(plan->boxes.size());
   return ok();
+}
+
+int ttb_emit_source(int kind_a, int kind_b, int rank, const int* perm, const int64_t* sizes,
+                    const int64_t* lda, const int64_t* ldb, double alpha, double beta, const char* plan_text,
+                    const char* basename, char* entry, size_t entry_len, char* header, size_t header_len,
+                    char* source, size_t source_len) {
+  return guarded([&] {
+    const Problem p = from_args(kind_a, kind_b, rank, perm, sizes, lda, ldb, alpha, beta);
+    check(p);
+    const Merged mg = fuse_indices(p);  // the reference emits for the normalized problem
+    const Problem& m = mg.p;
+    if (m.rank() > kMaxRank) return fail(TTB_EINVAL, "perm: rank after merging exceeds TTB_MAX_RANK");
+    Spec spec;
+    if (plan_text && *plan_text && !Spec::parse(plan_text, &spec))
+      return fail(TTB_EINVAL, "emit: cannot parse plan text");
+    if (!(plan_text && *plan_text)) spec.tx = spec.ty = 32;
+    const std::string sym = emit_entry_symbol(m);
+    const std::string base = basename && *basename ? basename : sym;
+    for (char ch : base)
+      if (!(std::isalnum(static_cast<unsigned char>(ch)) || ch == '_' || ch == '-' || ch == '.'))
+        return fail(TTB_EINVAL, "emit: basename must be a plain file name");
+    std::string h, s;
+    emit_cuda(m, make_geo(m), spec, base, spec.text(), cache_key(m), &h, &s);
+    const std::pair<const std::string*, std::pair<char*, size_t>> outs[] = {
+        {&sym, {entry, entry_len}}, {&h, {header, header_len}}, {&s, {source, source_len}}};
+    for (const auto& o : outs) {
+      if (!o.second.first) continue;
+      if (o.second.second <= o.first->size()) return fail(TTB_EINVAL, "emit: buffer too small");
+      std::memcpy(o.second.first, o.first->c_str(), o.first->size() + 1);
+    }
+    return ok();
+  });
 }
 
 int ttb_fill_uniform(int kind, int rank, const int64_t* sizes, const int64_t* ld,

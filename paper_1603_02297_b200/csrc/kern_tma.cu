@@ -3,6 +3,7 @@
 // run-chunk (case 1) consumers.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "dispatch.cuh"
@@ -27,6 +28,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return fn;
 }
 
+// L2 fetch size of the maps' loads (experiment switch TTB_TMA_L2: 0, 64, 128, 256)
+CUtensorMapL2promotion l2_promotion() {
+  static const CUtensorMapL2promotion p = [] {
+    const char* e = std::getenv("TTB_TMA_L2");
+    const int v = e ? std::atoi(e) : 256;
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                  : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                            : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
+  return p;
+}
+
 cudaError_t encode(CUtensorMap* m, const TmaView& v, const void* base) {
   PFN_cuTensorMapEncodeTiled_v12000 fn = encoder();
   if (!fn) return cudaErrorNotSupported;
@@ -41,7 +54,7 @@ cudaError_t encode(CUtensorMap* m, const TmaView& v, const void* base) {
   const CUresult r = fn(m, v.esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64,
                         static_cast<cuuint32_t>(v.rank), const_cast<void*>(base), dim, str, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 

@@ -879,7 +879,11 @@ void tma_candidates(const Geo& g, std::vector<Spec>* out) {
           if (sp.st < 2) continue;
           TmaPlan probe;
           if (!build_tma(g, sp, &probe, nullptr)) continue;
-          sp.cost = 1.5 + (1.0 - eff) * 12.0 + run_cost(run_a) + run_cost(run_b) + (odd ? 0.0 : 0.6) +
+          // measured (r02): with beta != 0 the tensor-map tile beats the bulk tile on
+          // every row it applies to (one load per side instead of a copy per
+          // row / column), with beta == 0 it trails it by 2-10%
+          sp.cost = (g.mode == 2 ? 0.5 : 1.5) + (1.0 - eff) * 12.0 + run_cost(run_a) + run_cost(run_b) +
+                    (odd ? 0.0 : 0.6) +
                     std::fabs(std::log2(static_cast<double>(tile) / (48.0 * 1024))) * 0.2 + 0.05 * (kx + ky);
           c.push_back(sp);
         }

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Summarize an ncu report (--set full) into the numbers the roofline needs.
 
-    python scripts/ncu_summary.py gpurun_out/prof.ncu-rep [--json out.json] [--bytes N]
+    python scripts/ncu_summary.py gpurun_out/prof.ncu-rep|raw.csv [--json out.json] [--bytes N]
 
 Prints per kernel launch: duration, DRAM read/write bytes (traffic), DRAM
 throughput, sectors per request (ld/st), shared-memory bank conflicts,
@@ -40,14 +40,19 @@ METRICS = {
     "block": ("launch__block_size", 1),
 }
 
-UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1,
-         "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9,
-         "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "B": 1, "KB": 1e3,
+         "MB": 1e6, "GB": 1e9}
+NANOSECONDS = {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3,
+               "ms": 1e6, "s": 1e9}
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    if rep.endswith(".csv"):  # `ncu -i X --page raw --csv` exported on the GPU box
+        with open(rep) as f:
+            out = f.read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return rows[0], rows[1], rows[2:]
 
@@ -70,11 +75,15 @@ def main():
                 v = float(row[i].replace(",", ""))
             except ValueError:
                 continue
-            u = units[i]
-            if key == "duration_us":
-                v = v * UNITS.get(u, 1) / 1e3
-            elif u in UNITS and "bytes" in key:
-                v = v * UNITS[u]
+            u = units[i].strip()
+            if key == "duration_us":  # to microseconds; an unknown unit is an error, not a guess
+                if u not in NANOSECONDS:
+                    raise ValueError(f"{name}: unknown time unit {u!r}")
+                v = v * NANOSECONDS[u] / 1e3
+            elif "bytes" in key:
+                if u not in BYTES:
+                    raise ValueError(f"{name}: unknown byte unit {u!r}")
+                v = v * BYTES[u]
             d[key] = v
         stalls = []
         for i, name in enumerate(hdr):

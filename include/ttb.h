@@ -218,9 +218,10 @@ int ttb_benchmark_manifest(int64_t volume_bytes, int kind, uint64_t seed, char* 
 
 /* ------------------------------------------- multi-GPU partitioning -- */
 
-/* Split B's outer index space for rank r of `world`: the
- * flattened range over B's k outermost merged indices, k the smallest with a
- * max/mean imbalance <= 1.05.  Writes *n_boxes <= 2*rank-1 boxes (origin +
+/* Split B's index space for rank r of `world`: the flattened
+ * range over the k slowest split axes -- B's indices from the outermost, with
+ * A's and B's stride-1 indices moved last (cutting them cuts the tiles' runs)
+ * -- k the smallest with a max/mean imbalance <= 1.05.  Writes *n_boxes <= 2*rank-1 boxes (origin +
  * extent, `rank` entries each in A index order, over the problem's index
  * space; pass NULL arrays to query the count); each box is an independent
  * sub-problem (same perm/lda/ldb, sizes = extent, buffers offset by origin). */

@@ -267,8 +267,15 @@ int execute(ttb_plan_s* pl, const Prepared& pr0, const void* A, void* B, cudaStr
   if (!aligned(B, pr->b_align)) return fail(TTB_EINVAL, "B buffer: misaligned for its element kind");
   Prepared run = *pr;
   run.cp.sc = run.rp.sc = run.sp.sc = run.tp.sc = Scale{alpha, beta};
+  // an error left behind by an unrelated earlier runtime call must not be
+  // reported as this launch's (cudaGetLastError after the launch reads it)
+  const cudaError_t stale = cudaGetLastError();
+  if (stale != cudaSuccess && cudaPeekAtLastError() != cudaSuccess)
+    return cuda_fail(stale, "before the kernel launch (sticky)");
   const cudaError_t e = launch(pl->geo, run, A, B, s);
-  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  if (e != cudaSuccess)
+    return cuda_fail(e, ("kernel launch (" + run.spec.text() + ", grid " + std::to_string(run.l.grid) + ", block " +
+                            std::to_string(run.l.block) + ", smem " + std::to_string(run.l.smem) + ")").c_str());
   return ok();
 }
 

@@ -43,7 +43,7 @@ struct BtileCfg {
     SmemParams q = p;
     q.ctr = btile_counter(s);  // null: static tile order
     return with(ka, kb, mode, jy, [&](auto fn) {
-      if (l.smem > 48 * 1024) {
+      if (l.smem > kSmemOptIn) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
         if (e != cudaSuccess) return e;
       }
@@ -57,7 +57,7 @@ struct BtileCfg {
     int n = 0;
     with(ka, kb, mode, jy, [&](auto fn) {
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (smem > kSmemOptIn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem);
     });
     return n;

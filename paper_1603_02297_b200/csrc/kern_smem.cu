@@ -68,7 +68,7 @@ cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Lau
   if (p.dense == 4) return launch_vtile(ka, kb, mode, p, l, s);
   if (p.dense == 5) return launch_btile(ka, kb, mode, p, l, s);
   return with_smem(ka, kb, mode, p.dense, p.ept, [&](auto fn) {
-    if (l.smem > 48 * 1024) {
+    if (l.smem > kSmemOptIn) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
       if (e != cudaSuccess) return e;
     }
@@ -83,7 +83,7 @@ int occupancy_smem(int ka, int kb, int mode, int dense, int ept, int block, int 
   with_smem(ka, kb, mode, dense, ept, [&](auto fn) {
     if (smem_carveout() >= 0)
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, smem_carveout());
-    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (smem > kSmemOptIn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem);
   });
   return n;

@@ -86,7 +86,7 @@ cudaError_t launch_tma(int ka, int kb, int mode, const TmaPlan& p, const void* A
   if (e == cudaSuccess) e = encode(&q.mb, p.vb, B);
   if (e != cudaSuccess) return e;
   return with_tma(ka, kb, mode, p.kch > 0, [&](auto fn) {
-    if (l.smem > 48 * 1024) {
+    if (l.smem > kSmemOptIn) {
       cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
       if (r != cudaSuccess) return r;
     }
@@ -100,7 +100,7 @@ int occupancy_tma(int ka, int kb, int mode, bool runs, int block, int smem) {
   int n = 0;
   with_tma(ka, kb, mode, runs, [&](auto fn) {
     cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (smem > kSmemOptIn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem);
   });
   return n;

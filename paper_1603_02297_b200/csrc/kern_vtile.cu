@@ -56,7 +56,7 @@ cudaError_t with_vtile(int ka, int kb, int mode, int va, int vb, int sh, F&& f) 
 cudaError_t launch_vtile(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                          cudaStream_t s) {
   return with_vtile(ka, kb, mode, p.va, p.vb, p.sh, [&](auto fn) {
-    if (l.smem > 48 * 1024) {
+    if (l.smem > kSmemOptIn) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);
       if (e != cudaSuccess) return e;
     }
@@ -71,7 +71,7 @@ int occupancy_vtile(int ka, int kb, int mode, int va, int vb, int sh, int block,
   with_vtile(ka, kb, mode, va, vb, sh, [&](auto fn) {
     if (smem_carveout() >= 0)
       cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, smem_carveout());
-    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (smem > kSmemOptIn) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem);
   });
   return n;

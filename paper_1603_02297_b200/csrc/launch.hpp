@@ -9,6 +9,10 @@
 
 namespace ttb {
 
+// dynamic shared memory above this opts in (cudaFuncAttributeMaxDynamicSharedMemorySize):
+// below 48 KB, with room for the kernels' static barriers and tables
+constexpr int kSmemOptIn = 40 * 1024;
+
 // mode: 0 move (alpha == 1, beta == 0), 1 scale (beta == 0), 2 update (beta != 0)
 cudaError_t launch_copy(int ka, int kb, int v, int mode, const CopyParams& p, const Launch& l,
                         cudaStream_t s);

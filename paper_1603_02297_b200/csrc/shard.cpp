@@ -3,9 +3,15 @@
 // Every element of B depends on exactly one element of A (executor.hpp:33-40),
 // so any partition of B's index space is independent: no exchange, no
 // collective on the data path.  Rank r receives a contiguous range of the
-// flattened index over B's k outermost positions, with k the smallest whose
-// extent product splits across `world` ranks within 5% of perfect balance.
-// The range decomposes into at most 2k-1 boxes of the original index space.
+// flattened index over the k slowest "split axes", with k the smallest whose
+// extent product splits across `world` ranks within 5% of perfect balance;
+// the range decomposes into at most 2k-1 boxes of the original index space.
+// Split axes are B's positions from the outermost, except that A's and B's
+// stride-1 axes come last: cutting either one cuts the contiguous runs the
+// tiles read and write (c5_t18's outermost B index is A's stride-1 axis of
+// extent 10 -- pieces of 1-2 elements -- measured 3.6x at 8 ranks instead of
+// 7x, scripts/predict_scaling.py).  A rank's B region is a slab whenever
+// B's outermost axis is eligible, which is the common case.
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -75,13 +81,23 @@ extern "C" int ttb_shard_boxes(int rank, const int* perm, const int64_t* sizes, 
     if (perm[a] < 1 || perm[a] > rank || inv[static_cast<size_t>(perm[a] - 1)] >= 0) return TTB_EINVAL;
     inv[static_cast<size_t>(perm[a] - 1)] = a;
   }
-  // B extents, outermost first
+  // split axes (A axis ids), slowest first: B positions outermost first,
+  // A's stride-1 axis (A axis 0) and B's (B position 0) moved to the end
+  std::vector<int> order;
+  for (int p = rank - 1; p >= 0; --p) {
+    const int a = inv[static_cast<size_t>(p)];
+    if (a != 0 && p != 0) order.push_back(a);
+  }
+  for (int p = rank - 1; p >= 0; --p) {
+    const int a = inv[static_cast<size_t>(p)];
+    if (a == 0 || p == 0) order.push_back(a);
+  }
   std::vector<int64_t> outer;
   int k = 0;
   int64_t F = 1;
-  for (int p = rank - 1; p >= 0; --p) {
-    F *= sizes[inv[static_cast<size_t>(p)]];
-    outer.push_back(sizes[inv[static_cast<size_t>(p)]]);
+  for (int a : order) {
+    F *= sizes[a];
+    outer.push_back(sizes[a]);
     ++k;
     const int64_t per = (F + world - 1) / world;
     if (static_cast<double>(per) * world / static_cast<double>(F) <= 1.05) break;
@@ -100,7 +116,7 @@ extern "C" int ttb_shard_boxes(int rank, const int* perm, const int64_t* sizes, 
       extents[i * rank + a] = sizes[a];
     }
     for (int j = 0; j < k; ++j) {
-      const int a = inv[static_cast<size_t>(rank - 1 - j)];
+      const int a = order[static_cast<size_t>(j)];
       origins[i * rank + a] = boxes[i].origin[static_cast<size_t>(j)];
       extents[i * rank + a] = boxes[i].extent[static_cast<size_t>(j)];
     }

@@ -146,3 +146,18 @@ def test_btile_plan_on_concurrent_streams():
     torch.cuda.synchronize()
     for o, w in zip(outs, wants):
         assert torch.equal(o, w)
+
+
+def test_dynamic_smem_just_under_48k_plus_static_barriers():
+    """A bulk tile whose ring takes 49,056 bytes of dynamic shared memory: with
+    the kernel's static mbarriers that exceeds 48 KB, so the launcher must opt
+    in (found by the sharded-execution test: 'invalid argument' at launch)."""
+    q = ttb.make_problem([2, 1], [50, 37], "c", "c", 1.0, 0.0, [101, 37], [37, 101])
+    plan = ttb.GpuPlan(q, cache=False)
+    plan.select("kern=smem;kx=1;ky=1;tx=50;ty=37;order=0;occ=0;st=3;bp=1;vec=3")
+    a = torch.rand(37 * 101 * 2, device="cuda")     # A[i1][i0][re/im], lda (101, 37)
+    b = torch.zeros(50 * 37 * 2, device="cuda")       # B[i0][i1][re/im], ldb (37, 101)
+    plan.execute(a, b)
+    torch.cuda.synchronize()
+    want = a.view(37, 101, 2)[:, :50].permute(1, 0, 2)
+    assert torch.equal(b.view(50, 37, 2), want)

@@ -359,18 +359,18 @@ def time_reference(slab_div: int, steps: int, warmup: int, threads: int, max_row
     for _ in range(warmup):
         for s, plan, _ in sessions:
             s.run(threads, plan)
-    per_step = []
+    # per row the minimum over the steps, as the reference's own timing
+    # protocol takes the minimum of its repetitions (tuner.hpp:14-18)
+    best = [float("inf")] * len(sessions)
     for _ in range(steps):
-        t = 0.0
-        for s, plan, _ in sessions:
-            t += s.run(threads, plan)
-        per_step.append(t)
+        for i, (s, plan, _) in enumerate(sessions):
+            best[i] = min(best[i], s.run(threads, plan))
     total_bytes = sum(b for _, _, b in sessions)
-    sec = statistics.median(per_step)
+    sec = sum(best)
     sample = (f"every c5 row, leading 1/{slab_div} slab of B's outermost index, "
               f"{len(sessions)} sub-problems, {total_bytes / 1e9:.2f} GB/step; per row the faster of "
               f"reference_transpose and execute_plan(tune cap {REF_TUNE_CAP}, d in {{0,5}}) "
-              f"({n_plan} rows took the tuned plan); median of {steps} steps")
+              f"({n_plan} rows took the tuned plan); per row the best of {steps} steps")
     for s, _, _ in sessions:
         s.close()
     return total_bytes / 1e9 / sec, sec, sample
@@ -608,7 +608,7 @@ def run_engine_arm(args):
             try:
                 if not _oracle().have_ref():
                     raise FileNotFoundError("oracle/_ref/libttune_ref.so not built")
-                gbs, sec, sample = time_reference(REF_SLAB_DIV, 3, 1, os.cpu_count() or 1)
+                gbs, sec, sample = time_reference(REF_SLAB_DIV, 5, 2, os.cpu_count() or 1)
                 line["cpu_baseline"] = {"value": round(gbs, 3), "unit": "GB/s",
                                         "cores": os.cpu_count() or 1, "kind": "reference",
                                         "cpu_model": cpu_model(), "sample": sample}

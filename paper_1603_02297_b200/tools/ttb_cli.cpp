@@ -5,7 +5,7 @@
 //
 //   ttb --perm=2,1 --size=7264,7264 [--dataType=s] [--alpha=1] [--beta=0]
 //       [--lda=..] [--ldb=..] [--cacheFile=F | $TTUNE_CACHE] [--hardwareKey=K]
-//       [--warmups=2] [--reps=3] [--seed=42] [--json]
+//       [--warmups=2] [--reps=3] [--seed=42] [--emit=BASE] [--json]
 //   ttb --benchmark [--volume=200] [--dataType=s] [--seed=42] [--manifest=F] [--json]
 //
 // Single mode: validate, look the problem up in the solution cache by
@@ -17,7 +17,8 @@
 // ("tunedGiBs"), CSV in the reference's columns or JSON.  CPU-search flags of
 // the reference (--prefetchDistances, --no-streaming-stores, --blockings,
 // --threads) are accepted and ignored; --maxImplementations caps the
-// candidates measured; --emit is not supported (exit 1).
+// candidates measured; --emit=BASE writes the solution's standalone sm_100a
+// kernel as BASE.cu plus its header next to it (pipeline.cpp:142-146, 182).
 // Exit codes as pipeline.cpp:189-200: 0 ok, 1 invalid argument, 2 other error.
 #include <cuda_runtime.h>
 
@@ -54,6 +55,7 @@ struct Config {
   uint64_t seed = 42;
   int warmups = 2, reps = 3;
   bool json = false;
+  std::string emit_base;
 };
 
 const char* kUsage =
@@ -127,7 +129,7 @@ int parse_args(int argc, char** argv, Config* c) {
     else if (a == "--warmups") c->warmups = static_cast<int>(parse_int(a, v));
     else if (a == "--reps") c->reps = static_cast<int>(parse_int(a, v));
     else if (a == "--json") c->json = true;
-    else if (a == "--emit") throw Invalid("--emit: source emission is not part of the GPU engine");
+    else if (a == "--emit") c->emit_base = v;
     else if (a == "--prefetchDistances" || a == "--blockings" || a == "--threads" ||
              a == "--no-streaming-stores") {
       // the reference's CPU search space; the GPU plan space replaces it
@@ -332,6 +334,24 @@ int run_single(const Config& c) {
     best = r.time(c.warmups, c.reps, &trials);
   }
   const std::string solution = r.describe();
+  std::string emitted_src, emitted_hdr;
+  if (!c.emit_base.empty()) {
+    // the solution's kernel as standalone source (emit_source + write_kernel_files)
+    const size_t slash = c.emit_base.find_last_of('/');
+    const std::string dir = slash == std::string::npos ? "" : c.emit_base.substr(0, slash + 1);
+    const std::string stem = slash == std::string::npos ? c.emit_base : c.emit_base.substr(slash + 1);
+    std::vector<char> hdr(1 << 14), src(1 << 17);
+    check(ttb_emit_source(ka, kb, r.rank, c.perm.data(), c.size.data(), pla, plb, c.alpha, c.beta,
+                          solution.c_str(), stem.c_str(), nullptr, 0, hdr.data(), hdr.size(), src.data(),
+                          src.size()));
+    emitted_src = c.emit_base + ".cu";
+    emitted_hdr = dir + stem + ".h";
+    for (const auto& f : {std::make_pair(emitted_src, src.data()), std::make_pair(emitted_hdr, hdr.data())}) {
+      std::ofstream out(f.first, std::ios::binary);
+      if (!out) throw std::runtime_error("emit: cannot write " + f.first);
+      out << f.second;
+    }
+  }
   if (c.json) {
     std::cout << "{\n  \"problemKey\": " << json_str(key) << ",\n  \"hardwareKey\": " << json_str(hw)
               << ",\n  \"cacheHit\": " << (hit ? "true" : "false")
@@ -341,7 +361,11 @@ int run_single(const Config& c) {
               << json_str(solution) << "},\n  \"bandwidthGiBs\": " << fmt(gibs, "%.17g")
               << ",\n  \"bestSeconds\": " << fmt(best, "%.17g") << ",\n  \"trialSeconds\": [";
     for (size_t i = 0; i < trials.size(); ++i) std::cout << (i ? ", " : "") << fmt(trials[i], "%.17g");
-    std::cout << "]\n}\n";
+    std::cout << "]";
+    if (!emitted_src.empty())
+      std::cout << ",\n  \"emitted\": {\"source\": " << json_str(emitted_src) << ", \"header\": "
+                << json_str(emitted_hdr) << "}";
+    std::cout << "\n}\n";
   } else {
     std::cout << "problem: " << key << "\n"
               << "merged: " << mkey << "\n"
@@ -350,6 +374,7 @@ int run_single(const Config& c) {
               << "candidates measured: " << measured << "\n"
               << "solution: " << solution << "\n"
               << "bandwidth: " << fmt(gibs) << " GiB/s\n";
+    if (!emitted_src.empty()) std::cout << "emitted: " << emitted_src << " " << emitted_hdr << "\n";
   }
   return 0;
 }

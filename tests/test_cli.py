@@ -34,8 +34,6 @@ def test_help_and_usage_errors():
     assert rc == 1 and "--size" in err
     rc, _, err = run("--perm", "2,1", "--size", "3,4", "--bogus=1")
     assert rc == 1 and "unknown option --bogus" in err
-    rc, _, err = run("--perm=2,1", "--size=3,4", "--emit=k")
-    assert rc == 1 and "emission" in err
 
 
 @pytest.mark.parametrize("args", [
@@ -81,6 +79,17 @@ def test_single_mode_miss_then_hit(tmp_path):
     assert lines["solution"].startswith(j["plan"]["serialized"].split(";fn=")[0])
     rc, out, _ = run(*args, env={"TTUNE_CACHE": cache})  # env default as the reference
     assert "cache: hit" in out
+    # --emit: the solution's standalone kernel next to its header (pipeline.cpp:142-146)
+    base = str(tmp_path / "out" / "k1")
+    os.makedirs(os.path.dirname(base))
+    rc, out, err = run(*args, f"--emit={base}", "--json")
+    assert rc == 0, err
+    j = json.loads(out)
+    assert j["emitted"] == {"source": base + ".cu", "header": base + ".h"}
+    src = open(base + ".cu").read()
+    assert '#include "k1.h"' in src and "plan: " in src
+    assert "void transpose_21_96x5600_dd(const double* A, double* B, double alpha, double beta);" \
+        in open(base + ".h").read()
 
 
 @pytest.mark.gpu

@@ -33,6 +33,8 @@
 // each), or from large tiles (kern_btile_big.cu) -- not from deeper rings.
 #pragma once
 
+#include <cuda.h>
+
 #include "kernels.cuh"
 
 namespace ttb {
@@ -87,6 +89,84 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// tensor-map box load (SASS UTMALDG) into shared memory, completion counted
+// in bytes on `bar`, and the box store (UTMASTG) in the thread's bulk group;
+// c[] holds one coordinate per map dim
+__device__ __forceinline__ void tma_load(const CUtensorMap* m, int rank, void* dst, const int* c,
+                                         uint64_t* bar) {
+  const uint32_t d = smem_u32(dst), b = smem_u32(bar);
+  const uint64_t mp = reinterpret_cast<uint64_t>(m);
+  switch (rank) {
+    case 1:
+      asm volatile(
+          "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];" ::"r"(d),
+          "l"(mp), "r"(c[0]), "r"(b)
+          : "memory");
+      break;
+    case 2:
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              d),
+          "l"(mp), "r"(c[0]), "r"(c[1]), "r"(b)
+          : "memory");
+      break;
+    case 3:
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+              d),
+          "l"(mp), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(b)
+          : "memory");
+      break;
+    case 4:
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+              d),
+          "l"(mp), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(b)
+          : "memory");
+      break;
+    default:
+      asm volatile(
+          "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(
+              d),
+          "l"(mp), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(b)
+          : "memory");
+      break;
+  }
+}
+
+__device__ __forceinline__ void tma_store(const CUtensorMap* m, int rank, const void* src, const int* c) {
+  const uint32_t s = smem_u32(src);
+  const uint64_t mp = reinterpret_cast<uint64_t>(m);
+  switch (rank) {
+    case 1:
+      asm volatile("cp.async.bulk.tensor.1d.global.shared::cta.bulk_group [%0, {%1}], [%2];" ::"l"(mp), "r"(c[0]),
+                   "r"(s)
+                   : "memory");
+      break;
+    case 2:
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(mp),
+                   "r"(c[0]), "r"(c[1]), "r"(s)
+                   : "memory");
+      break;
+    case 3:
+      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(mp),
+                   "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(s)
+                   : "memory");
+      break;
+    case 4:
+      asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(mp),
+                   "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(s)
+                   : "memory");
+      break;
+    default:
+      asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                       mp),
+                   "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(s)
+                   : "memory");
+      break;
+  }
+}
+
 // (stage layout: btile_stage_bytes, params.hpp)
 
 // P.ns stages, P.pa / P.pb row / column pitches (bytes), P.ly lanes along a
@@ -96,22 +176,32 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // when A's and B's stride-1 indices differ): an A tile row is then S*tx
 // elements, a B tile column S*ty.  MODE 0-3 as Update (3: B read directly
 // by the consumers, not through the ring).
+// kernel parameters: the tile plan plus, when P.tma is set, the tensor maps
+// of the side(s) that arrive as one box (param space, __grid_constant__)
+struct BtileParams {
+  CUtensorMap ma, mb;
+  SmemParams p;
+};
+
 template <class SA, class SB, int C, int MODE, int JY, int PW = kBtileProducerWarps,
           int NC = kBtileConsumerWarps>
-__global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams P) {
+__global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const __grid_constant__ BtileParams Q) {
+  const SmemParams& P = Q.p;
   using E = Vec<SA, C>;
   using EBv = Vec<SB, C>;
   constexpr uint32_t EA = sizeof(E), EB = sizeof(EBv);
   constexpr bool UPD = MODE == 2;  // B staged through the ring (MODE 3 reads B directly)
   // columns per consumer step: ~4 words of loads in flight per tile row
   constexpr int UX = EB <= 4 ? 4 : EB <= 8 ? 2 : 1;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full[kBtileMaxStages], empty[kBtileMaxStages];
 
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t NS = P.ns;
-  const uint32_t tables = btile_tables_bytes(P.tx, P.ty, UPD);
-  const uint32_t stage_bytes = btile_stage_bytes(P.tx, P.ty, P.pa, P.pb, UPD);
+  const uint32_t al = P.tma ? 128u : 16u;  // a box lands 128-byte aligned
+  const uint32_t tables = btile_tables_bytes(P.tx, P.ty, UPD, al);
+  const uint32_t stage_bytes = btile_stage_bytes(P.tx, P.ty, P.pa, P.pb, UPD, al);
+  const uint32_t a_bytes = btile_a_bytes(P.ty, P.pa, al);
   auto stage = [&](uint32_t s) { return smem_raw + s * stage_bytes; };
 
   if (tid == 0) {
@@ -162,8 +252,24 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
       uint32_t* boff = rbase + P.ty;
       uint32_t* cbase = boff + P.tx;
       unsigned char* ta = st + tables;
-      unsigned char* tb = ta + P.ty * P.pa;
+      unsigned char* tb = ta + a_bytes;
       uint32_t bytes = 0;
+      // a side that arrives by tensor map: one box, issued by the leader;
+      // the tile is dense in shared memory (rows of tx, columns of ty)
+      if (P.tma && leader) {
+        // dim 0 counts map elements: 16-byte kinds are two 8-byte ones
+        constexpr int SUBA = EA > 8 ? static_cast<int>(EA / 8) : 1, SUBB = EB > 8 ? static_cast<int>(EB / 8) : 1;
+        if (P.tma & 1) {
+          const int c[3] = {static_cast<int>(t.x0) * SUBA, static_cast<int>(t.y0), static_cast<int>(aO / P.tca)};
+          tma_load(&Q.ma, P.tra, ta, c, &full[s]);
+          bytes += P.tx * P.ty * EA;
+        }
+        if (UPD && (P.tma & 2)) {
+          const int c[3] = {static_cast<int>(t.y0) * SUBB, static_cast<int>(t.x0), static_cast<int>(bO / P.tcb)};
+          tma_load(&Q.mb, P.trb, tb, c, &full[s]);
+          bytes += P.tx * P.ty * EB;
+        }
+      }
       auto copy = [&](unsigned char* dst, uint64_t src, uint32_t n) {
         bulk_g2s(dst, reinterpret_cast<const void*>(src), n, &full[s]);
       };
@@ -207,7 +313,9 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
         bytes += static_cast<uint32_t>(hi - lo);
         tab[i] = (i * pitch + static_cast<uint32_t>(ga - lo)) / esz;
       };
-      if (P.runs & 1) {
+      if (P.tma & 1) {
+        for (uint32_t y = (warp - NC) * 32 + lane; y < t.ny; y += 32 * PW) rbase[y] = y * P.tx;
+      } else if (P.runs & 1) {
         for (uint32_t base = (warp - NC) * 32; base < t.ny; base += 32 * PW) {
           int64_t a = 0, b;
           const uint32_t y = base + lane;
@@ -221,7 +329,15 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
           fetch1(y, t.nx * P.S, a + aO + t.x0 * P.S, A, EA, ta, P.pa, rbase);
         }
       }
-      if (UPD && P.xp && t.nx == P.tx) {
+      if (UPD && (P.tma & 2)) {
+        // B box: column x at x*ty; the stores still need each column's offset
+        for (uint32_t x = (warp - NC) * 32 + lane; x < t.nx; x += 32 * PW) {
+          int64_t a, b;
+          decode(P.X, t.x0 + x, a, b);
+          boff[x] = static_cast<uint32_t>(b + bO + t.y0 * P.S);
+          cbase[x] = x * P.ty;
+        }
+      } else if (UPD && P.xp && t.nx == P.tx) {
         // column-permuted walk: fetch B columns in walk order j, where
         // consecutive columns continue each other in B
         for (uint32_t base = (warp - NC) * 32; base < t.nx; base += 32 * PW) {
@@ -278,7 +394,7 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const SmemParams 
     const uint32_t* boff = rbase + P.ty;
     const uint32_t* cbase = boff + P.tx;
     const E* ta = reinterpret_cast<const E*>(st + tables);
-    const EBv* tb = reinterpret_cast<const EBv*>(st + tables + P.ty * P.pa);
+    const EBv* tb = reinterpret_cast<const EBv*>(st + tables + a_bytes);
     if constexpr (JY == 0) {
       // linear walk of the tile in B order: element e of the tile index space
       // is column x = e / (S*ty), element c = e mod (S*ty) of that column; the

@@ -37,11 +37,20 @@ struct BtileCfg {
     });
   }
 
-  static cudaError_t launch(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
-                            cudaStream_t s) {
+  static cudaError_t launch(int ka, int kb, int mode, const SmemParams& p, const TmaPlan& tp,
+                            const Launch& l, cudaStream_t s) {
     const int jy = p.ly == 0 ? 0 : btile_rows_per_lane(p.S * p.ty, p.ly);  // ly 0: linear walk
-    SmemParams q = p;
-    q.ctr = btile_counter(s);  // null: static tile order
+    BtileParams q;
+    q.p = p;
+    q.p.ctr = btile_counter(s);  // null: static tile order
+    if (p.tma & 1) {
+      const cudaError_t e = tma_encode(&q.ma, tp.va, p.A);
+      if (e != cudaSuccess) return e;
+    }
+    if (p.tma & 2) {
+      const cudaError_t e = tma_encode(&q.mb, tp.vb, p.B);
+      if (e != cudaSuccess) return e;
+    }
     return with(ka, kb, mode, jy, [&](auto fn) {
       if (l.smem > kSmemOptIn) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);

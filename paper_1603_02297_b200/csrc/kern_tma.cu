@@ -40,7 +40,9 @@ CUtensorMapL2promotion l2_promotion() {
   return p;
 }
 
-cudaError_t encode(CUtensorMap* m, const TmaView& v, const void* base) {
+}  // namespace
+
+cudaError_t tma_encode(CUtensorMap* m, const TmaView& v, const void* base) {
   PFN_cuTensorMapEncodeTiled_v12000 fn = encoder();
   if (!fn) return cudaErrorNotSupported;
   cuuint64_t dim[kTmaMaxRank], str[kTmaMaxRank];
@@ -57,6 +59,8 @@ cudaError_t encode(CUtensorMap* m, const TmaView& v, const void* base) {
                         l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
+
+namespace {
 
 template <class F>
 cudaError_t with_tma(int ka, int kb, int mode, bool runs, F&& f) {
@@ -82,8 +86,8 @@ cudaError_t launch_tma(int ka, int kb, int mode, const TmaPlan& p, const void* A
                        cudaStream_t s) {
   TmaParams q;
   q.t = p;
-  cudaError_t e = encode(&q.ma, p.va, A);
-  if (e == cudaSuccess) e = encode(&q.mb, p.vb, B);
+  cudaError_t e = tma_encode(&q.ma, p.va, A);
+  if (e == cudaSuccess) e = tma_encode(&q.mb, p.vb, B);
   if (e != cudaSuccess) return e;
   return with_tma(ka, kb, mode, p.kch > 0, [&](auto fn) {
     if (l.smem > kSmemOptIn) {

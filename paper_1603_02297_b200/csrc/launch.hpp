@@ -1,6 +1,7 @@
 // launch.hpp -- host entry points into the templated kernels (kern_*.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -31,10 +32,10 @@ cudaError_t launch_vtile(int ka, int kb, int mode, const SmemParams& p, const La
 int occupancy_vtile(int ka, int kb, int mode, int va, int vb, int sh, int block, int smem);
 int smem_carveout();
 // btile_kernel (SmemParams::dense == 5, bulk-copy ring), kern_btile.cu
-cudaError_t launch_btile(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
+cudaError_t launch_btile(int ka, int kb, int mode, const SmemParams& p, const TmaPlan& tp, const Launch& l,
                          cudaStream_t s);
 int occupancy_btile(int ka, int kb, int mode, int jy, int block, int smem);
-cudaError_t launch_btile_big(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
+cudaError_t launch_btile_big(int ka, int kb, int mode, const SmemParams& p, const TmaPlan& tp, const Launch& l,
                              cudaStream_t s);
 int occupancy_btile_big(int ka, int kb, int mode, int jy, int block, int smem);
 // btile_kernel's tile counter [next, done] for one launch: the next slot of a
@@ -48,6 +49,8 @@ cudaError_t launch_tma(int ka, int kb, int mode, const TmaPlan& p, const void* A
                        cudaStream_t s);
 int occupancy_tma(int ka, int kb, int mode, bool runs, int block, int smem);
 bool tma_available();
+// encode one side's tensor map over `base` (kern_tma.cu)
+cudaError_t tma_encode(CUtensorMap* m, const TmaView& v, const void* base);
 
 // data utilities (util.cu)
 struct BoxParams {

@@ -131,6 +131,12 @@ struct SmemParams {
   unsigned int* ctr;       // dense == 5: [next tile, CTAs done] for dynamic tile scheduling, or null
   uint32_t xp, xm;         // dense == 5, linear walk: X0 extent and tx / xp (xp 0: natural column order)
   Div32 dxm;               // divisor xm
+  // dense == 5: bit 0 the A tile arrives as one tensor-map box [x0, y0, carrier]
+  // (X contiguous in A, one Y axis), bit 1 (beta != 0) the B tile as one box
+  // [y0, x0, carrier] (Y contiguous in B, one X axis); ranks of those maps and
+  // the element strides their carrier coordinates divide the outer offsets by
+  int tma, tra, trb;
+  int64_t tca, tcb;
 };
 
 // kTma: the tensor-map tile (tma.cuh).  One TMA box per tile and side: the A
@@ -183,18 +189,22 @@ constexpr int kBtileBigConsumerWarps = 8;
 constexpr int kBtileBigProducerWarps = 4;
 constexpr int kBtileBigTileBytes = 32 * 1024;
 
-// btile_kernel shared-memory layout of one stage (all offsets 16-byte aligned):
+// btile_kernel shared-memory layout of one stage (offsets multiples of `al`:
+// 16, or 128 when a tile side arrives by tensor map):
 //   header     u32 tile index of the stage (>= items: no more tiles), 16 bytes
 //   rbase[ty]  u32: element index of tile row y's first element in the A tile
 //   boff[tx]   u32: B element offset of tile column x's first element
 //   cbase[tx]  u32: (beta != 0) element index of column x in the B tile
 //   A tile     ty rows of pa bytes
 //   B tile     (beta != 0) tx columns of pb bytes
-TTB_HD uint32_t btile_tables_bytes(uint32_t tx, uint32_t ty, bool upd) {
-  return 16u + (((ty + tx * (upd ? 2u : 1u)) * 4u + 15u) & ~15u);  // 16: tile-index header
+TTB_HD uint32_t btile_round(uint32_t v, uint32_t al) { return (v + al - 1u) & ~(al - 1u); }
+TTB_HD uint32_t btile_tables_bytes(uint32_t tx, uint32_t ty, bool upd, uint32_t al = 16u) {
+  return btile_round(16u + (ty + tx * (upd ? 2u : 1u)) * 4u, al);  // 16: tile-index header
 }
-TTB_HD uint32_t btile_stage_bytes(uint32_t tx, uint32_t ty, uint32_t pa, uint32_t pb, bool upd) {
-  return btile_tables_bytes(tx, ty, upd) + ty * pa + (upd ? tx * pb : 0u);
+TTB_HD uint32_t btile_a_bytes(uint32_t ty, uint32_t pa, uint32_t al = 16u) { return btile_round(ty * pa, al); }
+TTB_HD uint32_t btile_stage_bytes(uint32_t tx, uint32_t ty, uint32_t pa, uint32_t pb, bool upd,
+                                  uint32_t al = 16u) {
+  return btile_round(btile_tables_bytes(tx, ty, upd, al) + btile_a_bytes(ty, pa, al) + (upd ? tx * pb : 0u), al);
 }
 
 // btile_kernel column elements per consumer lane (template JY: 1, 2, 4, 8 or 16)

@@ -165,6 +165,8 @@ uint32_t best_row_length(uint32_t S, uint32_t tx, uint32_t ty, int ebytes) {
 
 bool x_dense_in_a(const Geo& g, const std::vector<int>& xs, int64_t lead = 1);
 bool y_dense_in_b(const Geo& g, const std::vector<int>& ys, int64_t lead = 1);
+bool btile_tma_side(const Geo& g, bool a_side, const std::vector<int>& xs, const std::vector<int>& ys,
+                    uint32_t tx, uint32_t ty, TmaView* v, int64_t* carrier_stride, const char** why);
 
 // vector widths of vtile_kernel for a tile (false: element-wise only)
 bool vtile_widths(const Geo& g, const std::vector<int>& xs, const std::vector<int>& ys, int64_t tx,
@@ -487,6 +489,41 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
     for (const Spec& b : bulk_specs)
       if (b.bp == 0 && n < 2 && add(b)) ++n;
     for (const Spec& b : pick) out->push_back(b);
+    // the first picks again with the side(s) whose strides allow it arriving
+    // as one tensor-map box (fewer bulk copies per tile: the issue bound of
+    // the misaligned beta != 0 rows, btile.cuh)
+    if (!shared) {
+      int added = 0;
+      for (const Spec& b : pick) {
+        if (added >= 6 || b.xp) continue;
+        const std::vector<int> xs = x_group(0, b.kx), ys = y_group(g, 0, b.ky);
+        const uint32_t tx = static_cast<uint32_t>(std::min<int64_t>(b.tx, prod(g, xs)));
+        const uint32_t ty = static_cast<uint32_t>(std::min<int64_t>(b.ty, prod(g, ys)));
+        TmaView v;
+        int64_t cs;
+        const char* w = nullptr;
+        const bool b_ok = g.mode == 2 && b.bp == 1 && btile_tma_side(g, false, xs, ys, tx, ty, &v, &cs, &w);
+        // an A box lands dense: rows of an odd number of 16-byte chunks keep
+        // the column walk's lanes (one row each) off a single bank group
+        auto odd_rows = [&](uint32_t t) { return (t * static_cast<uint32_t>(g.eA)) % 32 == 16; };
+        uint32_t txa = tx;
+        for (uint32_t d = 0; d < 16 && !odd_rows(txa); ++d) {
+          const uint32_t lo = tx > d ? tx - d : 0, hi = tx + d;
+          if (lo >= 4 && odd_rows(lo)) txa = lo;
+          else if (hi <= prod(g, xs) && hi <= 256 && odd_rows(hi)) txa = hi;
+        }
+        const bool a_odd = odd_rows(txa) && btile_tma_side(g, true, xs, ys, txa, ty, &v, &cs, &w);
+        for (int ts : {1, 2, 3}) {
+          if (((ts & 1) && !a_odd) || ((ts & 2) && !b_ok)) continue;
+          Spec o = b;
+          o.ts = ts;
+          if (ts & 1) o.tx = static_cast<int>(txa);
+          o.cost -= 0.02;
+          out->push_back(o);
+          ++added;
+        }
+      }
+    }
     // and every pick with Y chunks fastest: tiles that share a B column's
     // ragged 32-byte sectors are then in flight together, so L2 merges the
     // partial writes instead of evicting them half-written
@@ -642,6 +679,73 @@ bool tma_view(const Geo& g, const int64_t* st, int e, const std::vector<int>& ti
   }
   if ((static_cast<uint64_t>(v->box[0]) * static_cast<uint64_t>(esz)) % 16) {
     *why = "tma: inner box not a multiple of 16 bytes";
+    return false;
+  }
+  return true;
+}
+
+// Tensor-map sides of a bulk tile (SmemParams::tma): bit 0 the A tile as one
+// box of A seen as [X (contiguous, one dim), Y0, carrier], bit 1 the B tile
+// (beta != 0) as one box of B seen as [Y (contiguous), X0, carrier]; the
+// carrier folds every other axis (the smallest of their strides divides the
+// others).  Strides must be multiples of 16 bytes, boxes at most 256.
+bool btile_tma_side(const Geo& g, bool a_side, const std::vector<int>& xs, const std::vector<int>& ys,
+                    uint32_t tx, uint32_t ty, TmaView* v, int64_t* carrier_stride, const char** why) {
+  const std::vector<int>& run = a_side ? xs : ys;    // contiguous group: dim 0
+  const std::vector<int>& other = a_side ? ys : xs;  // must be one axis: dim 1
+  const int64_t* st = a_side ? g.sa : g.sb;
+  const int e = a_side ? g.eA : g.eB;
+  if (other.size() != 1) {
+    *why = "smem: a tensor-map side needs a single-axis opposite group";
+    return false;
+  }
+  *v = TmaView{};
+  const int esz = e >= 8 ? 8 : 4;
+  const uint64_t sub = static_cast<uint64_t>(e / esz);
+  int64_t n0 = 1;
+  for (int a : run) n0 *= g.n[a];
+  const uint32_t b0 = a_side ? tx : ty, b1 = a_side ? ty : tx;
+  v->esz = esz;
+  v->rank = 2;
+  v->dim[0] = static_cast<uint64_t>(n0) * sub;
+  v->box[0] = static_cast<uint32_t>(b0 * sub);
+  v->dim[1] = static_cast<uint64_t>(g.n[other[0]]);
+  v->box[1] = b1;
+  v->stride[1] = static_cast<uint64_t>(st[other[0]]) * static_cast<uint64_t>(e);
+  int c = -1;
+  for (int a = 0; a < g.r; ++a) {
+    if (std::find(xs.begin(), xs.end(), a) != xs.end() || std::find(ys.begin(), ys.end(), a) != ys.end()) continue;
+    if (c < 0 || st[a] < st[c]) c = a;
+  }
+  *carrier_stride = 1;
+  if (c >= 0) {
+    uint64_t ext = 1;
+    for (int a = 0; a < g.r; ++a) {
+      if (std::find(xs.begin(), xs.end(), a) != xs.end() || std::find(ys.begin(), ys.end(), a) != ys.end()) continue;
+      if (st[a] % st[c]) {
+        *why = "smem: carrier stride does not divide";
+        return false;
+      }
+      ext += static_cast<uint64_t>(g.n[a] - 1) * static_cast<uint64_t>(st[a] / st[c]);
+    }
+    v->rank = 3;
+    v->dim[2] = ext;
+    v->box[2] = 1;
+    v->stride[2] = static_cast<uint64_t>(st[c]) * static_cast<uint64_t>(e);
+    *carrier_stride = st[c];
+  }
+  for (int k = 0; k < v->rank; ++k) {
+    if (v->box[k] < 1 || v->box[k] > 256 || v->dim[k] >= (uint64_t{1} << 31)) {
+      *why = "smem: tensor-map box or extent out of range";
+      return false;
+    }
+    if (k && (v->stride[k] % 16 || v->stride[k] >= (uint64_t{1} << 40))) {
+      *why = "smem: tensor-map stride not a multiple of 16 bytes";
+      return false;
+    }
+  }
+  if ((static_cast<uint64_t>(v->box[0]) * static_cast<uint64_t>(esz)) % 16) {
+    *why = "smem: tensor-map rows not a multiple of 16 bytes";
     return false;
   }
   return true;
@@ -964,6 +1068,7 @@ std::string Spec::text() const {
   std::string t = buf;
   if (v == kSmem && xp) t += ";xp=1";
   if (v == kSmem && ly) t += ";ly=" + std::to_string(ly);
+  if (v == kSmem && ts) t += ";ts=" + std::to_string(ts);
   return t;
 }
 
@@ -1024,6 +1129,8 @@ bool Spec::parse(const std::string& s, Spec* out) {
       p.ly = static_cast<int>(x);
     else if (k == "sb")
       p.sb = static_cast<int>(x);
+    else if (k == "ts")
+      p.ts = static_cast<int>(x);
     else
       return false;
   }
@@ -1395,6 +1502,23 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
       if ((m.pa / 16) % 2 == 0) m.pa += 16;
       m.pb = pitch(m.S * m.ty, g.eB);
       m.ns = static_cast<uint32_t>(s.st);
+      m.tma = m.tra = m.trb = 0;
+      m.tca = m.tcb = 1;
+      if (s.ts) {
+        // sides that arrive as one tensor-map box (dense tile, no row shifts)
+        const char* w = nullptr;
+        if (s.ts < 0 || s.ts > 3 || m.S != 1 || s.xp) return fail("smem: tensor-map sides not applicable");
+        if ((s.ts & 2) && g.mode != 2) return fail("smem: a B tensor-map side needs beta != 0");
+        if ((s.ts & 2) && s.bp == 0) return fail("smem: a B tensor-map side needs the B ring");
+        if ((s.ts & 1) && !btile_tma_side(g, true, xs, ys, m.tx, m.ty, &p.tp.va, &m.tca, &w)) return fail(w);
+        if ((s.ts & 2) && !btile_tma_side(g, false, xs, ys, m.tx, m.ty, &p.tp.vb, &m.tcb, &w)) return fail(w);
+        if (!tma_available()) return fail("smem: no tensor-map encoder in the driver");
+        m.tma = s.ts;
+        m.tra = p.tp.va.rank;
+        m.trb = p.tp.vb.rank;
+        if (s.ts & 1) m.pa = m.tx * static_cast<uint32_t>(g.eA);
+        if (s.ts & 2) m.pb = m.ty * static_cast<uint32_t>(g.eB);
+      }
     } else if (s.vec == 2) {
       if (!(s.st == 2 && small && m.S == 1 && vtile_shift(g, xs, ys, m.tx, m.ty, &va, &sh)))
         return fail("smem: shifted vector tile not applicable");
@@ -1431,7 +1555,8 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     if (g.mode == 2 && s.bp == 0 && m.dense) p.mode = 3;
     const auto r16 = [](int64_t v) { return (v + 15) & ~int64_t{15}; };
     const int64_t smem =
-        m.dense == 5 ? static_cast<int64_t>(m.ns) * btile_stage_bytes(m.tx, m.ty, m.pa, m.pb, p.mode == 2) :
+        m.dense == 5 ? static_cast<int64_t>(m.ns) * btile_stage_bytes(m.tx, m.ty, m.pa, m.pb, p.mode == 2,
+                                                                       m.tma ? 128u : 16u) :
         m.dense ? (m.dense == 3 ? 3 : 2) *  // pipeline stages (dense_stage_bytes in dense.cuh)
                       (r16(static_cast<int64_t>(m.tx + m.ty) * (m.dense >= 2 ? 4 : 8)) +
                        r16(static_cast<int64_t>(m.ty) * m.rl * g.eA) +

@@ -46,6 +46,7 @@ struct Spec {
   int xp = 0;          // smem, linear-walk bulk tile: walk X's second axis first (in the text only when 1)
   int ly = 0;          // smem, column-walk bulk tile: lanes along a column (0: up to 32; text only when set)
   int sb = 0;          // tma: B ring slots (0: as many as A stages `st`; text only when set)
+  int ts = 0;          // bulk tile: sides that arrive as one tensor-map box (1 A, 2 B; text only when set)
   double cost = 0;     // heuristic rank (lower first)
 
   std::string text() const;

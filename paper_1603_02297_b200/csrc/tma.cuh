@@ -42,81 +42,6 @@ struct TmaParams {
   TmaPlan t;
 };
 
-__device__ __forceinline__ void tma_load(const CUtensorMap* m, int rank, void* dst, const int* c,
-                                         uint64_t* bar) {
-  const uint32_t d = smem_u32(dst), b = smem_u32(bar);
-  const uint64_t mp = reinterpret_cast<uint64_t>(m);
-  switch (rank) {
-    case 1:
-      asm volatile(
-          "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];" ::"r"(d),
-          "l"(mp), "r"(c[0]), "r"(b)
-          : "memory");
-      break;
-    case 2:
-      asm volatile(
-          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-              d),
-          "l"(mp), "r"(c[0]), "r"(c[1]), "r"(b)
-          : "memory");
-      break;
-    case 3:
-      asm volatile(
-          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-              d),
-          "l"(mp), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(b)
-          : "memory");
-      break;
-    case 4:
-      asm volatile(
-          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
-              d),
-          "l"(mp), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(b)
-          : "memory");
-      break;
-    default:
-      asm volatile(
-          "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(
-              d),
-          "l"(mp), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(b)
-          : "memory");
-      break;
-  }
-}
-
-__device__ __forceinline__ void tma_store(const CUtensorMap* m, int rank, const void* src, const int* c) {
-  const uint32_t s = smem_u32(src);
-  const uint64_t mp = reinterpret_cast<uint64_t>(m);
-  switch (rank) {
-    case 1:
-      asm volatile("cp.async.bulk.tensor.1d.global.shared::cta.bulk_group [%0, {%1}], [%2];" ::"l"(mp), "r"(c[0]),
-                   "r"(s)
-                   : "memory");
-      break;
-    case 2:
-      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(mp),
-                   "r"(c[0]), "r"(c[1]), "r"(s)
-                   : "memory");
-      break;
-    case 3:
-      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(mp),
-                   "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(s)
-                   : "memory");
-      break;
-    case 4:
-      asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(mp),
-                   "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(s)
-                   : "memory");
-      break;
-    default:
-      asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
-                       mp),
-                   "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(s)
-                   : "memory");
-      break;
-  }
-}
-
 // tile index -> box coordinates of both maps (mixed-radix digits, each
 // feeding one dim of each map with a multiplier)
 __device__ __forceinline__ void tma_coords(const TmaPlan& P, uint32_t t, int* ca, int* cb) {

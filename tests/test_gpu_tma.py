@@ -126,3 +126,37 @@ def test_tma_not_offered_for_misaligned_strides():
         assert not t.startswith("kern=tma")
     with pytest.raises(ValueError, match="tma"):
         plan.select("kern=tma;kx=1;ky=1;tx=16;ty=16;order=0;occ=0;st=2")
+
+
+BTILE_CASES = CASES + [
+    ([2, 1], [516, 130], None, None),                 # B rows of 130: only A aligned (fp32)
+    ([2, 1], [130, 516], None, None),                 # only B aligned
+    ([3, 1, 2], [60, 7, 33], None, None),             # A lead 60, B lead 33
+]
+
+
+@pytest.mark.parametrize("ka,kb", PAIRS)
+def test_bulk_tile_tensor_map_sides_bit_exact(coracle, ka, kb):
+    """btile with the A tile and / or the B tile (beta != 0) arriving as one
+    tensor-map box (plan key ts=1|2|3) while the other side keeps its bulk
+    copies; every such candidate bit-exact."""
+    rng = np.random.default_rng(970 + kind_id(ka) * 4 + kind_id(kb))
+    n_run = 0
+    for perm, sizes, lda, ldb in BTILE_CASES:
+        if perm[0] == 1:
+            continue
+        for alpha, beta in [(1.0, 0.0), (0.7, 1.1)]:
+            p = ttb.make_problem(perm, sizes, ka, kb, alpha, beta, lda, ldb)
+            A, B = _inputs(coracle, rng, ka, kb, perm, sizes, lda, ldb, beta)
+            want = B.copy()
+            coracle.transpose(ka, kb, perm, sizes, lda, ldb, alpha, A, beta, want)
+            for text in [t for t in ttb.GpuPlan(p, cache=False).candidates() if ";ts=" in t]:
+                dA = torch.from_numpy(A.copy()).cuda()
+                dB = torch.from_numpy(B.copy()).cuda()
+                plan = ttb.GpuPlan(p, cache=False)
+                plan.select(text)
+                plan.execute(dA, dB)
+                torch.cuda.synchronize()
+                assert dB.cpu().numpy().tobytes() == want.tobytes(), (perm, sizes, alpha, beta, text)
+                n_run += 1
+    assert n_run > 0

@@ -1584,6 +1584,9 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     // compute the shift from element offsets, so the bases must be 16-B aligned
     p.a_align = m.sh ? 16 : std::min(16, g.eA * m.va);
     p.b_align = m.sh ? 16 : std::min(16, g.eB * m.vb);
+    // a tensor map's global address must be 16-byte aligned (else the fallback plan runs)
+    if (m.dense == 5 && (m.tma & 1)) p.a_align = 16;
+    if (m.dense == 5 && (m.tma & 2)) p.b_align = 16;
   }
   if (!(s.v == kSmem && p.sp.dense == 5)) p.l.block = 256;
   *out = p;

@@ -161,3 +161,32 @@ def test_dynamic_smem_just_under_48k_plus_static_barriers():
     torch.cuda.synchronize()
     want = a.view(37, 101, 2)[:, :50].permute(1, 0, 2)
     assert torch.equal(b.view(50, 37, 2), want)
+
+
+def test_every_plan_takes_the_fallback_on_misaligned_buffers():
+    """Buffers at a 4-byte offset (element-aligned, not 16): every candidate --
+    tensor-map tiles and bulk tiles with tensor-map sides included, whose maps
+    need 16-byte aligned bases -- must fall back and stay exact (found when
+    the sharded bench rows offset their sub-box pointers)."""
+    for perm, sizes, beta in [([2, 1], [516, 130], 0.5), ([2, 1], [130, 516], 0.5),
+                              ([3, 1, 2], [60, 20, 36], 0.0)]:
+        n = int(np.prod(sizes))
+        p = ttb.make_problem(perm, sizes, "s", "s", 1.0, beta)
+        a = torch.rand(n + 1, device="cuda")
+        b0 = torch.rand(n + 1, device="cuda")
+        sb = [sizes[perm.index(k + 1)] for k in range(len(sizes))]
+        at = a[1:].view(*reversed(sizes))
+        want = at.permute(*[len(sizes) - 1 - perm.index(len(sizes) - k) for k in range(len(sizes))])
+        want = want.contiguous().reshape(-1)
+        if beta:
+            want = want + beta * b0[1:]
+        plan = ttb.GpuPlan(p, cache=False)
+        texts = plan.candidates()
+        assert any("kern=tma" in t or "ts=" in t for t in texts)
+        for text in texts:
+            plan.select(text)
+            b = b0.clone()
+            plan.execute(a.data_ptr() + 4, b.data_ptr() + 4)
+            torch.cuda.synchronize()
+            assert torch.equal(b[1:], want), (perm, sizes, text)
+            assert b[0] == b0[0]

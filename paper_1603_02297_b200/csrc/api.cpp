@@ -238,7 +238,7 @@ cudaError_t launch(const Geo& g, Prepared pr, const void* A, void* B, cudaStream
     default:
       pr.sp.A = A;
       pr.sp.B = B;
-      if (pr.sp.dense == 5) return launch_btile(g.ka, g.kb, pr.mode, pr.sp, pr.tp, pr.l, s);
+      if (pr.sp.dense == 5) return launch_btile(g.ka, g.kb, pr.mode, pr.sp, pr.bt, pr.l, s);
       return launch_smem(g.ka, g.kb, pr.mode, pr.sp, pr.l, s);
   }
 }

@@ -179,7 +179,8 @@ __device__ __forceinline__ void tma_store(const CUtensorMap* m, int rank, const 
 // kernel parameters: the tile plan plus, when P.tma is set, the tensor maps
 // of the side(s) that arrive as one box (param space, __grid_constant__)
 struct BtileParams {
-  CUtensorMap ma, mb;
+  CUtensorMap ma[kBtileMaxClasses], mb[kBtileMaxClasses];  // per phase class (P.ca / P.cb)
+  int sha[kBtileMaxClasses], shb[kBtileMaxClasses];          // class row start within its 16 bytes (elements)
   SmemParams p;
 };
 
@@ -200,8 +201,11 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const __grid_cons
   const uint32_t NS = P.ns;
   const uint32_t al = P.tma ? 128u : 16u;  // a box lands 128-byte aligned
   const uint32_t tables = btile_tables_bytes(P.tx, P.ty, UPD, al);
-  const uint32_t stage_bytes = btile_stage_bytes(P.tx, P.ty, P.pa, P.pb, UPD, al);
-  const uint32_t a_bytes = btile_a_bytes(P.ty, P.pa, al);
+  const uint32_t stage_bytes = btile_stage_bytes(P.tx, P.ty, P.abytes, P.bbytes, UPD, al);
+  const uint32_t a_bytes = btile_round(P.abytes, al);
+  // tensor-map sides: elements per 16 bytes (box starts), class region sizes
+  constexpr uint32_t ALA = EA >= 16 ? 1u : 16u / EA, ALB = EB >= 16 ? 1u : 16u / EB;
+  const uint32_t cla = btile_class_bytes(P.rowa, P.cola, EA), clb = btile_class_bytes(P.rowb, P.colb, EB);
   auto stage = [&](uint32_t s) { return smem_raw + s * stage_bytes; };
 
   if (tid == 0) {
@@ -254,20 +258,34 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const __grid_cons
       unsigned char* ta = st + tables;
       unsigned char* tb = ta + a_bytes;
       uint32_t bytes = 0;
-      // a side that arrives by tensor map: one box, issued by the leader;
-      // the tile is dense in shared memory (rows of tx, columns of ty)
+      // a side that arrives by tensor map: per phase class r (rows y with
+      // y mod ca == r; one class when the rows are 16-byte aligned apart) one
+      // box of the class's rows in this tile, starting at the 16-byte aligned
+      // element at or before x0, issued by the leader
       if (P.tma && leader) {
         // dim 0 counts map elements: 16-byte kinds are two 8-byte ones
         constexpr int SUBA = EA > 8 ? static_cast<int>(EA / 8) : 1, SUBB = EB > 8 ? static_cast<int>(EB / 8) : 1;
         if (P.tma & 1) {
-          const int c[3] = {static_cast<int>(t.x0) * SUBA, static_cast<int>(t.y0), static_cast<int>(aO / P.tca)};
-          tma_load(&Q.ma, P.tra, ta, c, &full[s]);
-          bytes += P.tx * P.ty * EA;
+          for (uint32_t r = 0; r < P.ca; ++r) {
+            const uint32_t yr = t.y0 + (r + P.ca - t.y0 % P.ca) % P.ca;  // first row of class r
+            if (yr >= t.y0 + t.ny) continue;
+            const int x = static_cast<int>(t.x0) + Q.sha[r];
+            const int c[3] = {(x & ~static_cast<int>(ALA - 1)) * SUBA, static_cast<int>((yr - r) / P.ca),
+                              static_cast<int>(aO / P.tca)};
+            tma_load(&Q.ma[r], P.tra, ta + r * cla, c, &full[s]);
+            bytes += P.rowa * P.cola * EA;
+          }
         }
         if (UPD && (P.tma & 2)) {
-          const int c[3] = {static_cast<int>(t.y0) * SUBB, static_cast<int>(t.x0), static_cast<int>(bO / P.tcb)};
-          tma_load(&Q.mb, P.trb, tb, c, &full[s]);
-          bytes += P.tx * P.ty * EB;
+          for (uint32_t r = 0; r < P.cb; ++r) {
+            const uint32_t xr = t.x0 + (r + P.cb - t.x0 % P.cb) % P.cb;  // first column of class r
+            if (xr >= t.x0 + t.nx) continue;
+            const int y = static_cast<int>(t.y0) + Q.shb[r];
+            const int c[3] = {(y & ~static_cast<int>(ALB - 1)) * SUBB, static_cast<int>((xr - r) / P.cb),
+                              static_cast<int>(bO / P.tcb)};
+            tma_load(&Q.mb[r], P.trb, tb + r * clb, c, &full[s]);
+            bytes += P.rowb * P.colb * EB;
+          }
         }
       }
       auto copy = [&](unsigned char* dst, uint64_t src, uint32_t n) {
@@ -314,7 +332,12 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const __grid_cons
         tab[i] = (i * pitch + static_cast<uint32_t>(ga - lo)) / esz;
       };
       if (P.tma & 1) {
-        for (uint32_t y = (warp - NC) * 32 + lane; y < t.ny; y += 32 * PW) rbase[y] = y * P.tx;
+        for (uint32_t y = (warp - NC) * 32 + lane; y < t.ny; y += 32 * PW) {
+          const uint32_t yy = t.y0 + y, r = yy % P.ca;
+          const uint32_t yr = t.y0 + (r + P.ca - t.y0 % P.ca) % P.ca;
+          const uint32_t off = (t.x0 + static_cast<uint32_t>(Q.sha[r])) & (ALA - 1);
+          rbase[y] = r * (cla / EA) + (yy - yr) / P.ca * P.cola + off;
+        }
       } else if (P.runs & 1) {
         for (uint32_t base = (warp - NC) * 32; base < t.ny; base += 32 * PW) {
           int64_t a = 0, b;
@@ -335,7 +358,10 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const __grid_cons
           int64_t a, b;
           decode(P.X, t.x0 + x, a, b);
           boff[x] = static_cast<uint32_t>(b + bO + t.y0 * P.S);
-          cbase[x] = x * P.ty;
+          const uint32_t xx = t.x0 + x, r = xx % P.cb;
+          const uint32_t xr = t.x0 + (r + P.cb - t.x0 % P.cb) % P.cb;
+          const uint32_t off = (t.y0 + static_cast<uint32_t>(Q.shb[r])) & (ALB - 1);
+          cbase[x] = r * (clb / EB) + (xx - xr) / P.cb * P.colb + off;
         }
       } else if (UPD && P.xp && t.nx == P.tx) {
         // column-permuted walk: fetch B columns in walk order j, where

@@ -37,20 +37,35 @@ struct BtileCfg {
     });
   }
 
-  static cudaError_t launch(int ka, int kb, int mode, const SmemParams& p, const TmaPlan& tp,
+  // one phase class's map: its rows start `row` rows into the buffer; the
+  // map's base is the 16-byte aligned address at or before that, the shift
+  // (elements) tells the kernel where the rows begin inside a box
+  static cudaError_t encode_class(CUtensorMap* m, int* shift, TmaView v, const void* base, int64_t row_bytes,
+                                  uint32_t r, int e) {
+    const uintptr_t at = reinterpret_cast<uintptr_t>(base) + static_cast<uintptr_t>(row_bytes) * r;
+    const uintptr_t lo = at & ~static_cast<uintptr_t>(15);
+    *shift = static_cast<int>((at - lo) / static_cast<uintptr_t>(e));
+    const uint64_t per16 = 16u / static_cast<uint64_t>(v.esz);
+    v.dim[0] = (v.dim[0] + static_cast<uint64_t>(at - lo) / static_cast<uint64_t>(v.esz) + per16 - 1) / per16 * per16;
+    return tma_encode(m, v, reinterpret_cast<const void*>(lo));
+  }
+
+  static cudaError_t launch(int ka, int kb, int mode, const SmemParams& p, const BtileTma& bt,
                             const Launch& l, cudaStream_t s) {
     const int jy = p.ly == 0 ? 0 : btile_rows_per_lane(p.S * p.ty, p.ly);  // ly 0: linear walk
     BtileParams q;
     q.p = p;
     q.p.ctr = btile_counter(s);  // null: static tile order
-    if (p.tma & 1) {
-      const cudaError_t e = tma_encode(&q.ma, tp.va, p.A);
-      if (e != cudaSuccess) return e;
-    }
-    if (p.tma & 2) {
-      const cudaError_t e = tma_encode(&q.mb, tp.vb, p.B);
-      if (e != cudaSuccess) return e;
-    }
+    if (p.tma & 1)
+      for (uint32_t r = 0; r < p.ca; ++r) {
+        const cudaError_t e = encode_class(&q.ma[r], &q.sha[r], bt.a[r], p.A, bt.row_bytes_a, r, bt.ea);
+        if (e != cudaSuccess) return e;
+      }
+    if (p.tma & 2)
+      for (uint32_t r = 0; r < p.cb; ++r) {
+        const cudaError_t e = encode_class(&q.mb[r], &q.shb[r], bt.b[r], p.B, bt.row_bytes_b, r, bt.eb);
+        if (e != cudaSuccess) return e;
+      }
     return with(ka, kb, mode, jy, [&](auto fn) {
       if (l.smem > kSmemOptIn) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, l.smem);

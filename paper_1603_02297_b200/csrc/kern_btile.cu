@@ -57,11 +57,11 @@ unsigned int* btile_counter(cudaStream_t) {
 
 using BtileSmall = BtileCfg<kBtileConsumerWarps, kBtileProducerWarps, 0, 1, 2, 4, 8, 16>;
 
-cudaError_t launch_btile(int ka, int kb, int mode, const SmemParams& p, const TmaPlan& tp, const Launch& l,
+cudaError_t launch_btile(int ka, int kb, int mode, const SmemParams& p, const BtileTma& bt, const Launch& l,
                          cudaStream_t s) {
   if (l.block == 32 * (kBtileBigConsumerWarps + kBtileBigProducerWarps))
-    return launch_btile_big(ka, kb, mode, p, tp, l, s);
-  return BtileSmall::launch(ka, kb, mode, p, tp, l, s);
+    return launch_btile_big(ka, kb, mode, p, bt, l, s);
+  return BtileSmall::launch(ka, kb, mode, p, bt, l, s);
 }
 
 int occupancy_btile(int ka, int kb, int mode, int jy, int block, int smem) {

@@ -8,9 +8,9 @@ namespace ttb {
 
 using BtileBig = BtileCfg<kBtileBigConsumerWarps, kBtileBigProducerWarps, 2, 4, 8>;
 
-cudaError_t launch_btile_big(int ka, int kb, int mode, const SmemParams& p, const TmaPlan& tp, const Launch& l,
+cudaError_t launch_btile_big(int ka, int kb, int mode, const SmemParams& p, const BtileTma& bt, const Launch& l,
                              cudaStream_t s) {
-  return BtileBig::launch(ka, kb, mode, p, tp, l, s);
+  return BtileBig::launch(ka, kb, mode, p, bt, l, s);
 }
 
 int occupancy_btile_big(int ka, int kb, int mode, int jy, int block, int smem) {

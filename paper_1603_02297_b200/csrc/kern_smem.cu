@@ -66,7 +66,7 @@ int smem_carveout() {
 cudaError_t launch_smem(int ka, int kb, int mode, const SmemParams& p, const Launch& l,
                         cudaStream_t s) {
   if (p.dense == 4) return launch_vtile(ka, kb, mode, p, l, s);
-  if (p.dense == 5 && !p.tma) return launch_btile(ka, kb, mode, p, TmaPlan{}, l, s);
+  if (p.dense == 5 && !p.tma) return launch_btile(ka, kb, mode, p, BtileTma{}, l, s);
   if (p.dense == 5) return cudaErrorInvalidValue;  // tensor-map sides: launch_btile with the plan's views
   return with_smem(ka, kb, mode, p.dense, p.ept, [&](auto fn) {
     if (l.smem > kSmemOptIn) {

@@ -32,10 +32,10 @@ cudaError_t launch_vtile(int ka, int kb, int mode, const SmemParams& p, const La
 int occupancy_vtile(int ka, int kb, int mode, int va, int vb, int sh, int block, int smem);
 int smem_carveout();
 // btile_kernel (SmemParams::dense == 5, bulk-copy ring), kern_btile.cu
-cudaError_t launch_btile(int ka, int kb, int mode, const SmemParams& p, const TmaPlan& tp, const Launch& l,
+cudaError_t launch_btile(int ka, int kb, int mode, const SmemParams& p, const BtileTma& bt, const Launch& l,
                          cudaStream_t s);
 int occupancy_btile(int ka, int kb, int mode, int jy, int block, int smem);
-cudaError_t launch_btile_big(int ka, int kb, int mode, const SmemParams& p, const TmaPlan& tp, const Launch& l,
+cudaError_t launch_btile_big(int ka, int kb, int mode, const SmemParams& p, const BtileTma& bt, const Launch& l,
                              cudaStream_t s);
 int occupancy_btile_big(int ka, int kb, int mode, int jy, int block, int smem);
 // btile_kernel's tile counter [next, done] for one launch: the next slot of a

@@ -131,12 +131,18 @@ struct SmemParams {
   unsigned int* ctr;       // dense == 5: [next tile, CTAs done] for dynamic tile scheduling, or null
   uint32_t xp, xm;         // dense == 5, linear walk: X0 extent and tx / xp (xp 0: natural column order)
   Div32 dxm;               // divisor xm
-  // dense == 5: bit 0 the A tile arrives as one tensor-map box [x0, y0, carrier]
-  // (X contiguous in A, one Y axis), bit 1 (beta != 0) the B tile as one box
-  // [y0, x0, carrier] (Y contiguous in B, one X axis); ranks of those maps and
-  // the element strides their carrier coordinates divide the outer offsets by
+  // dense == 5: bit 0 the A tile arrives by tensor map, bit 1 (beta != 0) the B
+  // tile.  A side: A seen as [X (contiguous, one dim), Y0, carrier]; when Y0's
+  // stride is not a multiple of 16 bytes its rows split into `ca` phase
+  // classes (y mod ca), each a map whose rows are 16-byte aligned apart, one
+  // box per class per tile ([cola, rowa, 1]) landing in its own region of the
+  // tile; B side likewise over columns ([colb, rowb, 1], `cb` classes).
+  // Ranks of the maps and the element strides their carrier coordinates
+  // divide the outer offsets by.
   int tma, tra, trb;
   int64_t tca, tcb;
+  uint32_t ca, cola, rowa, cb, colb, rowb;
+  uint32_t abytes, bbytes;  // dense == 5: bytes of the A tile / B tile regions of a stage
 };
 
 // kTma: the tensor-map tile (tma.cuh).  One TMA box per tile and side: the A
@@ -176,6 +182,15 @@ struct TmaPlan {
   uint32_t kch;
   Div32 dk, dby;
 };
+// the tensor-map sides of a bulk tile: per side up to 4 phase-class maps
+constexpr int kBtileMaxClasses = 4;
+struct BtileTma {
+  // per class; dim[0] holds the row length (map elements) before the launch
+  // adds the class's start shift and rounds up to 16 bytes
+  TmaView a[kBtileMaxClasses], b[kBtileMaxClasses];
+  int64_t row_bytes_a = 0, row_bytes_b = 0;  // A stride of Y0 / B stride of X0 (class r starts r rows in)
+  int ea = 4, eb = 4;                        // tensor element bytes of A / B
+};
 constexpr int kTmaConsumerWarps = 4;
 constexpr int kTmaStoreWarps = 2;
 
@@ -202,9 +217,12 @@ TTB_HD uint32_t btile_tables_bytes(uint32_t tx, uint32_t ty, bool upd, uint32_t 
   return btile_round(16u + (ty + tx * (upd ? 2u : 1u)) * 4u, al);  // 16: tile-index header
 }
 TTB_HD uint32_t btile_a_bytes(uint32_t ty, uint32_t pa, uint32_t al = 16u) { return btile_round(ty * pa, al); }
-TTB_HD uint32_t btile_stage_bytes(uint32_t tx, uint32_t ty, uint32_t pa, uint32_t pb, bool upd,
+// a side by tensor map: `classes` boxes of rows x cols elements of e bytes, each 128-byte aligned
+TTB_HD uint32_t btile_class_bytes(uint32_t rows, uint32_t cols, uint32_t e) { return btile_round(rows * cols * e, 128u); }
+// abytes / bbytes: the A tile / B tile regions (SmemParams::abytes, bbytes)
+TTB_HD uint32_t btile_stage_bytes(uint32_t tx, uint32_t ty, uint32_t abytes, uint32_t bbytes, bool upd,
                                   uint32_t al = 16u) {
-  return btile_round(btile_tables_bytes(tx, ty, upd, al) + btile_a_bytes(ty, pa, al) + (upd ? tx * pb : 0u), al);
+  return btile_round(btile_tables_bytes(tx, ty, upd, al) + btile_round(abytes, al) + (upd ? bbytes : 0u), al);
 }
 
 // btile_kernel column elements per consumer lane (template JY: 1, 2, 4, 8 or 16)

@@ -165,8 +165,13 @@ uint32_t best_row_length(uint32_t S, uint32_t tx, uint32_t ty, int ebytes) {
 
 bool x_dense_in_a(const Geo& g, const std::vector<int>& xs, int64_t lead = 1);
 bool y_dense_in_b(const Geo& g, const std::vector<int>& ys, int64_t lead = 1);
+struct TmaSide {
+  uint32_t classes = 1, cols = 0, rows = 0;
+  int rank = 0;
+  int64_t carrier_stride = 1;
+};
 bool btile_tma_side(const Geo& g, bool a_side, const std::vector<int>& xs, const std::vector<int>& ys,
-                    uint32_t tx, uint32_t ty, TmaView* v, int64_t* carrier_stride, const char** why);
+                    uint32_t tx, uint32_t ty, BtileTma* bt, TmaSide* out, const char** why);
 
 // vector widths of vtile_kernel for a tile (false: element-wise only)
 bool vtile_widths(const Geo& g, const std::vector<int>& xs, const std::vector<int>& ys, int64_t tx,
@@ -499,10 +504,9 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
         const std::vector<int> xs = x_group(0, b.kx), ys = y_group(g, 0, b.ky);
         const uint32_t tx = static_cast<uint32_t>(std::min<int64_t>(b.tx, prod(g, xs)));
         const uint32_t ty = static_cast<uint32_t>(std::min<int64_t>(b.ty, prod(g, ys)));
-        TmaView v;
-        int64_t cs;
+        TmaSide sd;
         const char* w = nullptr;
-        const bool b_ok = g.mode == 2 && b.bp == 1 && btile_tma_side(g, false, xs, ys, tx, ty, &v, &cs, &w);
+        const bool b_ok = g.mode == 2 && b.bp == 1 && btile_tma_side(g, false, xs, ys, tx, ty, nullptr, &sd, &w);
         // an A box lands dense: rows of an odd number of 16-byte chunks keep
         // the column walk's lanes (one row each) off a single bank group
         auto odd_rows = [&](uint32_t t) { return (t * static_cast<uint32_t>(g.eA)) % 32 == 16; };
@@ -512,9 +516,9 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
           if (lo >= 4 && odd_rows(lo)) txa = lo;
           else if (hi <= prod(g, xs) && hi <= 256 && odd_rows(hi)) txa = hi;
         }
-        const bool a_odd = odd_rows(txa) && btile_tma_side(g, true, xs, ys, txa, ty, &v, &cs, &w);
+        const bool a_ok = odd_rows(txa) && btile_tma_side(g, true, xs, ys, txa, ty, nullptr, &sd, &w);
         for (int ts : {1, 2, 3}) {
-          if (((ts & 1) && !a_odd) || ((ts & 2) && !b_ok)) continue;
+          if (((ts & 1) && !a_ok) || ((ts & 2) && !b_ok)) continue;
           Spec o = b;
           o.ts = ts;
           if (ts & 1) o.tx = static_cast<int>(txa);
@@ -684,13 +688,18 @@ bool tma_view(const Geo& g, const int64_t* st, int e, const std::vector<int>& ti
   return true;
 }
 
-// Tensor-map sides of a bulk tile (SmemParams::tma): bit 0 the A tile as one
-// box of A seen as [X (contiguous, one dim), Y0, carrier], bit 1 the B tile
-// (beta != 0) as one box of B seen as [Y (contiguous), X0, carrier]; the
-// carrier folds every other axis (the smallest of their strides divides the
-// others).  Strides must be multiples of 16 bytes, boxes at most 256.
+// Tensor-map sides of a bulk tile (SmemParams::tma): bit 0 the A tile by
+// maps of A seen as [X (contiguous, one dim), Y0, carrier], bit 1 (beta != 0)
+// the B tile by maps of B seen as [Y (contiguous), X0, carrier]; the carrier
+// folds every other axis (the smallest of their strides divides the others).
+// When the opposite axis' stride is not a multiple of 16 bytes its rows split
+// into `classes` = 16 / gcd(stride bytes, 16) phase classes (row mod classes),
+// each a map whose rows are classes * stride apart (a multiple of 16 bytes)
+// from a base rounded down to 16 bytes; a class box is `rows` rows of `cols`
+// elements, cols covering the tile row from the 16-byte aligned element at or
+// before it.  Strides of the carrier must be multiples of 16 bytes.
 bool btile_tma_side(const Geo& g, bool a_side, const std::vector<int>& xs, const std::vector<int>& ys,
-                    uint32_t tx, uint32_t ty, TmaView* v, int64_t* carrier_stride, const char** why) {
+                    uint32_t tx, uint32_t ty, BtileTma* bt, TmaSide* out, const char** why) {
   const std::vector<int>& run = a_side ? xs : ys;    // contiguous group: dim 0
   const std::vector<int>& other = a_side ? ys : xs;  // must be one axis: dim 1
   const int64_t* st = a_side ? g.sa : g.sb;
@@ -699,55 +708,85 @@ bool btile_tma_side(const Geo& g, bool a_side, const std::vector<int>& xs, const
     *why = "smem: a tensor-map side needs a single-axis opposite group";
     return false;
   }
-  *v = TmaView{};
   const int esz = e >= 8 ? 8 : 4;
-  const uint64_t sub = static_cast<uint64_t>(e / esz);
+  const uint32_t sub = static_cast<uint32_t>(e / esz);
+  const uint32_t al = e >= 16 ? 1u : 16u / static_cast<uint32_t>(e);  // elements per 16 bytes
   int64_t n0 = 1;
   for (int a : run) n0 *= g.n[a];
-  const uint32_t b0 = a_side ? tx : ty, b1 = a_side ? ty : tx;
-  v->esz = esz;
-  v->rank = 2;
-  v->dim[0] = static_cast<uint64_t>(n0) * sub;
-  v->box[0] = static_cast<uint32_t>(b0 * sub);
-  v->dim[1] = static_cast<uint64_t>(g.n[other[0]]);
-  v->box[1] = b1;
-  v->stride[1] = static_cast<uint64_t>(st[other[0]]) * static_cast<uint64_t>(e);
-  int c = -1;
-  for (int a = 0; a < g.r; ++a) {
-    if (std::find(xs.begin(), xs.end(), a) != xs.end() || std::find(ys.begin(), ys.end(), a) != ys.end()) continue;
-    if (c < 0 || st[a] < st[c]) c = a;
+  const int64_t n1 = g.n[other[0]];
+  const uint64_t row_bytes = static_cast<uint64_t>(st[other[0]]) * static_cast<uint64_t>(e);
+  uint64_t gcd = 16;
+  while (row_bytes % gcd) gcd /= 2;
+  TmaSide sd;
+  sd.classes = static_cast<uint32_t>(16 / gcd);
+  // Phase classes (rows not 16-byte aligned apart) work -- each class box
+  // reads its rows from the 16-byte boundary before them -- but measured
+  // slower than the bulk copies on every misaligned c5 row (t22: 4.75 vs
+  // 5.74 TB/s): the over-read crosses into another 128-byte line on most
+  // rows.  Likewise a box wider than the tile.  So a side qualifies only with
+  // aligned rows, tile rows of whole 16-byte chunks and (ts plans require it)
+  // a 16-byte aligned base.
+  if (sd.classes != 1) {
+    *why = "smem: tensor-map side rows not 16-byte aligned apart";
+    return false;
   }
-  *carrier_stride = 1;
+  const uint32_t b0 = a_side ? tx : ty, b1 = a_side ? ty : tx;
+  if (b0 % al) {
+    *why = "smem: tensor-map side rows not whole 16-byte chunks";
+    return false;
+  }
+  sd.rows = b1;
+  sd.cols = b0;
+  int c = -1;
+  auto in_tile = [&](int a) {
+    return std::find(xs.begin(), xs.end(), a) != xs.end() || std::find(ys.begin(), ys.end(), a) != ys.end();
+  };
+  for (int a = 0; a < g.r; ++a)
+    if (!in_tile(a) && (c < 0 || st[a] < st[c])) c = a;
+  uint64_t cext = 1;
   if (c >= 0) {
-    uint64_t ext = 1;
     for (int a = 0; a < g.r; ++a) {
-      if (std::find(xs.begin(), xs.end(), a) != xs.end() || std::find(ys.begin(), ys.end(), a) != ys.end()) continue;
+      if (in_tile(a)) continue;
       if (st[a] % st[c]) {
         *why = "smem: carrier stride does not divide";
         return false;
       }
-      ext += static_cast<uint64_t>(g.n[a] - 1) * static_cast<uint64_t>(st[a] / st[c]);
+      cext += static_cast<uint64_t>(g.n[a] - 1) * static_cast<uint64_t>(st[a] / st[c]);
     }
-    v->rank = 3;
-    v->dim[2] = ext;
-    v->box[2] = 1;
-    v->stride[2] = static_cast<uint64_t>(st[c]) * static_cast<uint64_t>(e);
-    *carrier_stride = st[c];
+    sd.carrier_stride = st[c];
   }
-  for (int k = 0; k < v->rank; ++k) {
-    if (v->box[k] < 1 || v->box[k] > 256 || v->dim[k] >= (uint64_t{1} << 31)) {
-      *why = "smem: tensor-map box or extent out of range";
-      return false;
+  sd.rank = c >= 0 ? 3 : 2;
+  for (uint32_t r = 0; r < sd.classes; ++r) {
+    TmaView v;
+    v.esz = esz;
+    v.rank = sd.rank;
+    v.dim[0] = static_cast<uint64_t>(n0) * sub;  // the launch adds the class's shift and rounds up
+    v.box[0] = sd.cols * sub;
+    v.dim[1] = static_cast<uint64_t>(std::max<int64_t>(1, (n1 - static_cast<int64_t>(r) + sd.classes - 1) / sd.classes));
+    v.box[1] = sd.rows;
+    v.stride[1] = row_bytes * sd.classes;
+    if (c >= 0) {
+      v.dim[2] = cext;
+      v.box[2] = 1;
+      v.stride[2] = static_cast<uint64_t>(st[c]) * static_cast<uint64_t>(e);
     }
-    if (k && (v->stride[k] % 16 || v->stride[k] >= (uint64_t{1} << 40))) {
-      *why = "smem: tensor-map stride not a multiple of 16 bytes";
-      return false;
+    for (int k = 0; k < v.rank; ++k) {
+      if (v.box[k] < 1 || v.box[k] > 256 || v.dim[k] + 16 >= (uint64_t{1} << 31)) {
+        *why = "smem: tensor-map box or extent out of range";
+        return false;
+      }
+      if (k && (v.stride[k] % 16 || v.stride[k] >= (uint64_t{1} << 40))) {
+        *why = "smem: tensor-map stride not a multiple of 16 bytes";
+        return false;
+      }
     }
+    if (bt) (a_side ? bt->a : bt->b)[r] = v;
   }
-  if ((static_cast<uint64_t>(v->box[0]) * static_cast<uint64_t>(esz)) % 16) {
-    *why = "smem: tensor-map rows not a multiple of 16 bytes";
-    return false;
+  if (bt) {
+    (a_side ? bt->row_bytes_a : bt->row_bytes_b) = static_cast<int64_t>(row_bytes);
+    (a_side ? bt->ea : bt->eb) = e;
   }
+  *out = sd;
   return true;
 }
 
@@ -1504,20 +1543,37 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
       m.ns = static_cast<uint32_t>(s.st);
       m.tma = m.tra = m.trb = 0;
       m.tca = m.tcb = 1;
+      m.ca = m.cb = 1;
+      m.cola = m.rowa = m.colb = m.rowb = 0;
+      m.abytes = m.ty * m.pa;
+      m.bbytes = m.tx * m.pb;
       if (s.ts) {
-        // sides that arrive as one tensor-map box (dense tile, no row shifts)
+        // sides that arrive by tensor map (phase-class boxes, btile.cuh)
         const char* w = nullptr;
         if (s.ts < 0 || s.ts > 3 || m.S != 1 || s.xp) return fail("smem: tensor-map sides not applicable");
         if ((s.ts & 2) && g.mode != 2) return fail("smem: a B tensor-map side needs beta != 0");
         if ((s.ts & 2) && s.bp == 0) return fail("smem: a B tensor-map side needs the B ring");
-        if ((s.ts & 1) && !btile_tma_side(g, true, xs, ys, m.tx, m.ty, &p.tp.va, &m.tca, &w)) return fail(w);
-        if ((s.ts & 2) && !btile_tma_side(g, false, xs, ys, m.tx, m.ty, &p.tp.vb, &m.tcb, &w)) return fail(w);
+        TmaSide sa, sb;
+        if ((s.ts & 1) && !btile_tma_side(g, true, xs, ys, m.tx, m.ty, &p.bt, &sa, &w)) return fail(w);
+        if ((s.ts & 2) && !btile_tma_side(g, false, xs, ys, m.tx, m.ty, &p.bt, &sb, &w)) return fail(w);
         if (!tma_available()) return fail("smem: no tensor-map encoder in the driver");
         m.tma = s.ts;
-        m.tra = p.tp.va.rank;
-        m.trb = p.tp.vb.rank;
-        if (s.ts & 1) m.pa = m.tx * static_cast<uint32_t>(g.eA);
-        if (s.ts & 2) m.pb = m.ty * static_cast<uint32_t>(g.eB);
+        if (s.ts & 1) {
+          m.tra = sa.rank;
+          m.tca = sa.carrier_stride;
+          m.ca = sa.classes;
+          m.cola = sa.cols;
+          m.rowa = sa.rows;
+          m.abytes = sa.classes * btile_class_bytes(sa.rows, sa.cols, static_cast<uint32_t>(g.eA));
+        }
+        if (s.ts & 2) {
+          m.trb = sb.rank;
+          m.tcb = sb.carrier_stride;
+          m.cb = sb.classes;
+          m.colb = sb.cols;
+          m.rowb = sb.rows;
+          m.bbytes = sb.classes * btile_class_bytes(sb.rows, sb.cols, static_cast<uint32_t>(g.eB));
+        }
       }
     } else if (s.vec == 2) {
       if (!(s.st == 2 && small && m.S == 1 && vtile_shift(g, xs, ys, m.tx, m.ty, &va, &sh)))
@@ -1555,7 +1611,7 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     if (g.mode == 2 && s.bp == 0 && m.dense) p.mode = 3;
     const auto r16 = [](int64_t v) { return (v + 15) & ~int64_t{15}; };
     const int64_t smem =
-        m.dense == 5 ? static_cast<int64_t>(m.ns) * btile_stage_bytes(m.tx, m.ty, m.pa, m.pb, p.mode == 2,
+        m.dense == 5 ? static_cast<int64_t>(m.ns) * btile_stage_bytes(m.tx, m.ty, m.abytes, m.bbytes, p.mode == 2,
                                                                        m.tma ? 128u : 16u) :
         m.dense ? (m.dense == 3 ? 3 : 2) *  // pipeline stages (dense_stage_bytes in dense.cuh)
                       (r16(static_cast<int64_t>(m.tx + m.ty) * (m.dense >= 2 ? 4 : 8)) +
@@ -1584,7 +1640,8 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     // compute the shift from element offsets, so the bases must be 16-B aligned
     p.a_align = m.sh ? 16 : std::min(16, g.eA * m.va);
     p.b_align = m.sh ? 16 : std::min(16, g.eB * m.vb);
-    // a tensor map's global address must be 16-byte aligned (else the fallback plan runs)
+    // a tensor-map side's map starts at the buffer: 16-byte aligned bases
+    // (a misaligned buffer takes the fallback plan)
     if (m.dense == 5 && (m.tma & 1)) p.a_align = 16;
     if (m.dense == 5 && (m.tma & 2)) p.b_align = 16;
   }

@@ -62,6 +62,7 @@ struct Prepared {
   RtParams rp{};
   SmemParams sp{};
   TmaPlan tp{};
+  BtileTma bt{};  // bulk tile: the tensor-map sides' class views
   int a_align = 1, b_align = 1;  // required base alignment (bytes) of A and B
 };
 

@@ -104,6 +104,12 @@ int main() {
       // partial box at the end (OOB fill)
       {"oob", 2, {50, 40}, {64}, {16, 8}, {40, 36}, CU_TENSOR_MAP_SWIZZLE_NONE},
       // swizzle 128B with a 32-byte inner box (layout printed)
+      // a box whose dim-0 start is not 16-byte aligned (coordinate 1, 3, 5)
+      {"start1", 2, {4000, 4000}, {4000}, {36, 20}, {1, 5}, CU_TENSOR_MAP_SWIZZLE_NONE},
+      {"start3", 2, {4003, 4000}, {4000}, {40, 4}, {3, 7}, CU_TENSOR_MAP_SWIZZLE_NONE},
+      {"start5", 3, {1001, 20, 40}, {1004, 1004 * 20}, {8, 3, 2}, {5, 4, 3}, CU_TENSOR_MAP_SWIZZLE_NONE},
+      // a row stride of 4 elements' phase: class view (every 4th row, base at row 1)
+      {"classrow", 2, {283 + 3, 100}, {283 * 4}, {96, 8}, {3, 2}, CU_TENSOR_MAP_SWIZZLE_NONE},
       // 4D non-monotone
       {"nonmono4", 4, {8, 16, 16, 16}, {8 * 16 * 16, 8, 8 * 16}, {8, 4, 4, 2}, {0, 1, 2, 3},
        CU_TENSOR_MAP_SWIZZLE_NONE},

@@ -25,6 +25,7 @@ cudaError_t with_copy(int ka, int kb, int v, int mode, bool long_rows, F&& f) {
 
 cudaError_t launch_copy(int ka, int kb, int v, int mode, const CopyParams& p, const Launch& l,
                         cudaStream_t s) {
+  if (p.bulk) return launch_rowcopy(ka, kb, mode, p, l, s);
   return with_copy(ka, kb, v, mode, p.long_rows != 0, [&](auto fn) {
     fn<<<l.grid, l.block, 0, s>>>(p);
     count_launch();

@@ -86,6 +86,12 @@ struct alignas((sizeof(T) * N) >= 16 ? 16 : (sizeof(T) * N)) Vec {
   T v[N];
 };
 
+// N elements moved as one aligned unit (16 or 32 bytes: LDS/STS/STG.128)
+template <class T, int N>
+struct alignas(16) Piece {
+  T e[N];
+};
+
 // streaming read-only load of one <=16-byte chunk (A is never written)
 template <int BYTES>
 __device__ __forceinline__ void ld_nc(const void* p, void* out) {

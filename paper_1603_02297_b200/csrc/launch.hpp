@@ -52,6 +52,10 @@ bool tma_available();
 // encode one side's tensor map over `base` (kern_tma.cu)
 cudaError_t tma_encode(CUtensorMap* m, const TmaView& v, const void* base);
 
+// rowcopy_kernel (CopyParams::bulk), kern_rows.cu
+cudaError_t launch_rowcopy(int ka, int kb, int mode, const CopyParams& p, const Launch& l, cudaStream_t s);
+int occupancy_rowcopy(int ka, int kb, int mode, int block, int smem);
+
 // data utilities (util.cu)
 struct BoxParams {
   int rank = 0;

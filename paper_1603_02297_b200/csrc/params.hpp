@@ -76,7 +76,26 @@ struct CopyParams {
   uint32_t items;         // warp items: long rows (row, segment); short rows 32-row groups
   int long_rows;          // 1: copy_rows_kernel, 0: copy_kernel
   int align;              // copy_rows_kernel: segments on 128-byte lines of B (1) or A (2), 0 off
+  // rowcopy_kernel (bulk rows): a row in segments of `bseg` elements, each
+  // brought into shared memory by one bulk copy (its 16-byte aligned
+  // superset) and written out with 16-byte stores at B's alignment; `bns`
+  // ring stages of `bstage` bytes; items = rows * bnseg
+  // rows shorter than a segment travel `brows` at a time (one copy each)
+  int bulk;
+  uint32_t bseg, bnseg, brows, bns, bstage, bitems;
+  Div32 dbnseg;
 };
+constexpr int kRowsConsumerWarps = 4;
+constexpr int kRowsMaxGroup = 32;
+// rowcopy_kernel stage: `rows` 32-byte headers (128-byte multiple), then per
+// row an A slot of `seg` elements (+16 for the aligned superset), then (beta
+// != 0) the B slots; slot bytes 16-byte multiples
+TTB_HD uint32_t rowcopy_slot_bytes(uint32_t seg, uint32_t e) { return (seg * e + 16u + 15u) & ~15u; }
+TTB_HD uint32_t rowcopy_head_bytes(uint32_t rows) { return (rows * 32u + 127u) & ~127u; }
+TTB_HD uint32_t rowcopy_stage_bytes(uint32_t seg, uint32_t rows, uint32_t ea, uint32_t eb, bool upd) {
+  return (rowcopy_head_bytes(rows) + rows * (rowcopy_slot_bytes(seg, ea) + (upd ? rowcopy_slot_bytes(seg, eb) : 0u)) +
+          127u) & ~127u;
+}
 
 // kRt: register micro-tile transpose between the X space (starts with A's
 // stride-1 axis) and the Y space (starts with B's stride-1 axis), vectors of

@@ -1108,6 +1108,7 @@ std::string Spec::text() const {
   if (v == kSmem && xp) t += ";xp=1";
   if (v == kSmem && ly) t += ";ly=" + std::to_string(ly);
   if (v == kSmem && ts) t += ";ts=" + std::to_string(ts);
+  if (v == kCopy && bulk) t += ";bulk=" + std::to_string(bulk) + ";st=" + std::to_string(st);
   return t;
 }
 
@@ -1170,6 +1171,8 @@ bool Spec::parse(const std::string& s, Spec* out) {
       p.sb = static_cast<int>(x);
     else if (k == "ts")
       p.ts = static_cast<int>(x);
+    else if (k == "bulk")
+      p.bulk = static_cast<int>(x);
     else
       return false;
   }
@@ -1217,6 +1220,15 @@ std::vector<Spec> candidates(const Geo& g) {
           a.order = al << 1;
           a.cost += 0.01 * al;
           out.push_back(a);
+        }
+      }
+      if (w == 1 && g.n[0] * emax >= 1024) {  // bulk rows (rows.cuh): any alignment, bytes in flight in smem
+        for (auto kb_st : {std::pair<int, int>{16, 4}, {32, 3}, {8, 6}}) {
+          Spec r = b;
+          r.bulk = kb_st.first;
+          r.st = kb_st.second;
+          r.cost = cost - 0.2 + 0.01 * (kb_st.first != 16);
+          out.push_back(r);
         }
       }
       for (auto t : {std::pair<int, int>{1, 1}, {8, 8}, {4, 16}, {16, 4}, {32, 1}, {2, 2}}) {
@@ -1311,7 +1323,7 @@ std::vector<Spec> candidates(const Geo& g) {
   Spec fallback;
   bool have_fb = false;
   for (const Spec& s : out)
-    if (!have_fb && ((s.v == kSmem && s.vec < 3) || (s.v == kCopy && s.w1 == 1))) {
+    if (!have_fb && ((s.v == kSmem && s.vec < 3) || (s.v == kCopy && s.w1 == 1 && !s.bulk))) {
       fallback = s;
       fallback.vec = 0;
       fallback.xp = 0;
@@ -1389,10 +1401,12 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     const uint64_t rows = uint64_t{c.nxc} * c.nyc * c.O.total * c.tx * c.ty;  // incl. masked
     // vectors per warp item of copy_rows_kernel (4 KB of the row)
     const uint32_t kSeg = 32u * static_cast<uint32_t>(rows_item_vectors(v * std::max(g.eA, g.eB)));
-    c.long_rows = c.lvec >= 128 ? 1 : 0;
+    // order bit 3 keeps mid-length rows (128+ vectors) on the 32-rows-per-warp
+    // kernel: a row of a few KB leaves most of a 4 KB long-row item idle
+    c.long_rows = c.lvec >= 128 && !(s.order & 8) ? 1 : 0;
     // long rows: segments aligned to 128-byte lines of one side (one more
     // segment per row for the shortened first one)
-    c.align = c.long_rows ? s.order >> 1 : 0;
+    c.align = c.long_rows ? (s.order >> 1) & 3 : 0;
     c.nseg = (c.lvec + kSeg - 1 + (c.align ? 128 : 0)) / kSeg;
     c.dseg = Div32::make(c.nseg);
     // warp items: (row, segment) for long rows, groups of 32 rows for short ones
@@ -1408,6 +1422,38 @@ bool prepare(const Geo& g, const Spec& s, int sms, Prepared* out, std::string* w
     p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, int64_t{occ} * sms)));
     p.a_align = v * g.eA;
     p.b_align = v * g.eB;
+    c.bulk = 0;
+    c.bseg = c.bnseg = c.bns = c.bstage = c.bitems = 0;
+    c.dbnseg = Div32::make(1);
+    if (s.bulk) {
+      // bulk rows (rows.cuh): segments of s.bulk KB, any element alignment
+      if (v != 1 || s.bulk < 1 || s.bulk > 64) return fail("copy: bulk rows need v=1 and 1..64 KB segments");
+      if (s.st < 2 || s.st > 8) return fail("copy: bulk row stages outside 2..8");
+      c.bulk = 1;
+      c.bseg = static_cast<uint32_t>(s.bulk * 1024 / std::max(g.eA, g.eB));
+      c.bnseg = (c.lvec + c.bseg - 1) / c.bseg;
+      // one row (segment) per stage: packing several short rows per stage
+      // (c.brows > 1, supported by the kernel) measured slower on every
+      // shape tried -- the single producer lane serialises their copies
+      c.brows = 1;
+      const uint64_t bitems = (uint64_t{c.rows} + c.brows - 1) / c.brows * c.bnseg;
+      if (bitems >= kIdxLimit) return fail("copy: too many row segments");
+      c.bitems = static_cast<uint32_t>(bitems);
+      c.dbnseg = Div32::make(c.bnseg);
+      c.bns = static_cast<uint32_t>(s.st);
+      c.bstage = rowcopy_stage_bytes(std::min(c.bseg, c.lvec), c.brows, static_cast<uint32_t>(g.eA),
+                                     static_cast<uint32_t>(g.eB), g.mode == 2);
+      const int64_t smem = int64_t{c.bns} * c.bstage;
+      if (smem > 200 * 1024) return fail("copy: bulk row stages do not fit shared memory");
+      p.l.smem = static_cast<int>(smem);
+      p.l.block = 32 * (kRowsConsumerWarps + 1);
+      const int occr = std::min(occ_cap, std::max(1, occupancy_rowcopy(g.ka, g.kb, g.mode, p.l.block, p.l.smem)));
+      p.l.grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(c.bitems, int64_t{occr} * sms)));
+      p.a_align = g.eA;
+      p.b_align = g.eB;
+      *out = p;
+      return true;
+    }
   } else if (s.v == kRt) {
     if (g.pos[0] == 0) return fail("rt: stride-1 index is not transposed");
     const int y_first = g.at[0];

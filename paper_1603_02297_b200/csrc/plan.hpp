@@ -47,6 +47,7 @@ struct Spec {
   int ly = 0;          // smem, column-walk bulk tile: lanes along a column (0: up to 32; text only when set)
   int sb = 0;          // tma: B ring slots (0: as many as A stages `st`; text only when set)
   int ts = 0;          // bulk tile: sides that arrive as one tensor-map box (1 A, 2 B; text only when set)
+  int bulk = 0;        // copy: bulk rows in segments of this many KB (rowcopy_kernel, `st` stages; text only when set)
   double cost = 0;     // heuristic rank (lower first)
 
   std::string text() const;

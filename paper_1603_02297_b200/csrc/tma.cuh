@@ -83,10 +83,6 @@ __device__ __forceinline__ void tma_lane(uint32_t lane, uint32_t wxl, uint32_t& 
   }
 }
 
-template <class T, int N>
-struct alignas(16) Piece {
-  T e[N];
-};
 
 template <class SA, class SB, int C, int MODE, bool RUNS, int NC = kTmaConsumerWarps,
           int SW = kTmaStoreWarps>

@@ -113,6 +113,9 @@ PROBES: List[Workload] = [
     Workload("p_lrow_0", "d", (0, 2, 1), (324360, 60, 10), 1.0, 0.0, 7012),
     Workload("p_mrow_b", "d", (0, 2, 1), (8192, 160, 150), 1.0, 0.5, 7013, 7014),
     Workload("p_srow_b", "d", (0, 2, 1), (1024, 400, 475), 1.0, 0.5, 7015, 7016),
+    # the suite's slowest case (d3_132_balanced, 200 MiB fp32, alpha = beta = 1):
+    # case-1 rows of 375 floats (1500 bytes) at alternating 16-byte phases
+    Workload("p_suite_d3_132", "s", (0, 2, 1), (375, 375, 373), 1.0, 1.0, 7017, 7018),
 ]
 
 BY_NAME = {w.name: w for w in ALL + PROBES}

@@ -211,6 +211,8 @@ struct BtileTma {
   int ea = 4, eb = 4;                        // tensor element bytes of A / B
 };
 constexpr int kTmaConsumerWarps = 4;
+// TmaPlan::wxl value of the diagonal lane map (8 x 8 micro-tile blocks, half per warp step)
+constexpr uint32_t kTmaDiagonal = 6;
 constexpr int kTmaStoreWarps = 2;
 
 // btile_kernel warp roles: consumer warps write B; producer warps issue the

@@ -913,15 +913,18 @@ bool build_tma(const Geo& g, const Spec& s, TmaPlan* tp, std::string* why) {
     t.my = static_cast<uint32_t>(BY / wm);
     // warp tiles of 4 x 8 micro-tiles (the conflict-free lane map), or wider
     // ones when the tile is short along y (fewer idle lanes)
-    t.wxl = 2;
+    // (16-byte kinds keep the 4 x 8 map: conflict-free when bx is odd)
+    t.wxl = wm >= 2 ? kTmaDiagonal : 2;
     auto util = [&](uint32_t l) {
-      const uint32_t wx = 1u << l, wy = 32u >> l;
+      const uint32_t wx = l == kTmaDiagonal ? 8u : 1u << l, wy = l == kTmaDiagonal ? 8u : 32u >> l;
       return static_cast<double>(t.mx) * t.my / (((t.mx + wx - 1) / wx) * wx * (((t.my + wy - 1) / wy) * wy));
     };
     for (uint32_t l : {3u, 4u, 5u})
       if (util(l) > util(t.wxl) * 1.25) t.wxl = l;
-    t.nwx = (t.mx + (1u << t.wxl) - 1) >> t.wxl;
-    t.nwt = t.nwx * ((t.my + (32u >> t.wxl) - 1) / (32u >> t.wxl));
+    const bool diag = t.wxl == kTmaDiagonal;
+    const uint32_t wx = diag ? 8u : 1u << t.wxl, wy = diag ? 8u : 32u >> t.wxl;
+    t.nwx = (t.mx + wx - 1) / wx;
+    t.nwt = t.nwx * ((t.my + wy - 1) / wy) * (diag ? 2u : 1u);
     t.dnwx = Div32::make(t.nwx);
   }
   return true;

@@ -69,7 +69,10 @@ __device__ __forceinline__ void tma_coords(const TmaPlan& P, uint32_t t, int* ca
 // w = 2, and the stores the same with i and j swapped.
 template <int WM>
 __device__ __forceinline__ void tma_lane(uint32_t lane, uint32_t wxl, uint32_t& i, uint32_t& j) {
-  if (wxl != 2) {  // warp tiles of 8, 16 or 32 micro-tiles along x (short tiles along y)
+  if (wxl == kTmaDiagonal) {  // i = k (x within the 8 x 8 block), j = d (the lane's diagonal)
+    i = lane & 7;
+    j = lane >> 3;
+  } else if (wxl != 2) {  // warp tiles of 8, 16 or 32 micro-tiles along x (short tiles along y)
     i = lane & ((1u << wxl) - 1);
     j = lane >> wxl;
   } else if constexpr (WM == 1) {
@@ -199,11 +202,17 @@ __global__ void __launch_bounds__(32 * (NC + 2 + SW)) tma_kernel(const __grid_co
         *dst = b;
       }
     } else {
-      const uint32_t wxn = 1u << P.wxl, wyn = 32u >> P.wxl;
+      const bool diag = P.wxl == kTmaDiagonal;
+      const uint32_t wxn = diag ? 8u : 1u << P.wxl, wyn = diag ? 8u : 32u >> P.wxl;
       for (uint32_t w = cw; w < P.nwt; w += NC) {
-        const uint32_t wy = udiv(w, P.dnwx);
-        const uint32_t wx = w - wy * P.nwx;
-        const uint32_t xb = wxn * wx + i, ya = wyn * wy + j;
+        const uint32_t blk = diag ? w >> 1 : w;
+        const uint32_t wy = udiv(blk, P.dnwx);
+        const uint32_t wx = blk - wy * P.nwx;
+        uint32_t xb = wxn * wx + i, ya = wyn * wy + j;
+        // diagonal map: an 8-lane phase holds (x + k, y + (k + d) mod 8), k = 0..7,
+        // distinct x for the loads and distinct y for the stores whatever the
+        // row lengths (bank group k (W q + 1) + const with W q even, likewise W p)
+        if (diag) ya = wyn * wy + ((i + 4 * (w & 1) + j) & 7);
         if (xb >= P.mx || ya >= P.my) continue;
         // WM rows of the A tile (y = WM*ya + r), WM elements each (x = WM*xb + q)
         Piece<EA, WM> a[WM];

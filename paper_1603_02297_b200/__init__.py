@@ -453,7 +453,14 @@ class GpuPlan:
         check(lib.ttb_plan_execute(self._h, C.c_void_p(pa), C.c_void_p(pb), _stream(stream)))
 
     def execute_host(self, a_host, b_host) -> None:
-        """End-to-end on host (numpy/pinned torch) buffers: H2D, kernel, D2H."""
+        """End-to-end on host (numpy/pinned torch) buffers: H2D, kernel, D2H.
+        Both buffers are sized like execute's (the C ABI cannot size them)."""
+        p = self.problem
+        for name, buf, kind, need in (("A", a_host, p.kind_a, required_elements_a(p)),
+                                      ("B", b_host, p.kind_b, required_elements_b(p))):
+            nbytes = buf.nbytes if hasattr(buf, "nbytes") else buf.numel() * buf.element_size()
+            if nbytes < need * kind.bytes:
+                raise ValueError(f"{name} buffer: too small for problem")
         pa = a_host.ctypes.data if hasattr(a_host, "ctypes") else a_host.data_ptr()
         pb = b_host.ctypes.data if hasattr(b_host, "ctypes") else b_host.data_ptr()
         check(lib.ttb_plan_execute_host(self._h, C.c_void_p(pa), C.c_void_p(pb)))

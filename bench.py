@@ -426,7 +426,8 @@ def measure_d2d(torch):
 
 
 def bench_configs(torch, ttb, peak, d2d):
-    """c1-c4s at full size on one GPU: autotuned plan, best of 5 (tuner.hpp:14-18)."""
+    """c1-c4s at full size on one GPU: autotuned plan, best of 10 after 5 warm-ups (the
+    reference takes minima of repetitions too, tuner.hpp:14-18; 70-300 us kernels)."""
     from paper_1603_02297_b200.workloads import CONFIGS
     golden = golden_checksums()
     out = {}
@@ -444,10 +445,10 @@ def bench_configs(torch, ttb, peak, d2d):
         plan.execute(a, b)
         ok = ttb.checksum(w.kind, w.sizes_b, w.ldb and list(w.ldb), b.data_ptr()) == golden[w.name]
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-        for _ in range(3):
+        for _ in range(5):
             plan.execute(a, b)
         best = 1e30
-        for _ in range(5):
+        for _ in range(10):
             e0.record()
             plan.execute(a, b)
             e1.record()

@@ -234,6 +234,8 @@ __global__ void __launch_bounds__(32 * (NC + PW)) btile_kernel(const __grid_cons
       mbar_wait(&empty[s], ph ^ 1);  // a fresh barrier passes parity 1 at once
       unsigned char* st = stage(s);
       volatile uint32_t* hdr = reinterpret_cast<volatile uint32_t*>(st);
+      // (claiming the next tile one round early, to hide the counter's round
+      // trip, measured 1% slower on c5_t00 / t13: the claim is not the bound)
       if (k > 0) it = P.ctr ? (leader ? g + atomicAdd(P.ctr, 1u) : 0u) : it + g;
       if (leader) *hdr = it;
       asm volatile("bar.sync 1, %0;" ::"r"(32 * PW) : "memory");

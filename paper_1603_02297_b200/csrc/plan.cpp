@@ -262,7 +262,7 @@ bool y_dense_in_b(const Geo& g, const std::vector<int>& ys, int64_t lead) {
 
 // staged-tile candidates over every admissible pair of X / Y groups
 void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
-  std::vector<Spec> bulk_specs;
+  std::vector<Spec> bulk_specs, whole_specs, whole_box;
   std::vector<Spec>* bulk = &bulk_specs;
   const int start = shared ? 1 : 0;
   if (g.r <= start) return;
@@ -308,6 +308,13 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
               const int64_t t = (N + k - 1) / k;
               if (t >= 16 && t <= cap && std::find(v.begin(), v.end(), t) == v.end()) v.push_back(t);
             }
+          // and of a long group: the side nearest below 64 / 128 / 256 that
+          // splits it evenly (2695 -> 22 x 123 instead of 21 x 128 + 7)
+          for (int64_t target : {64, 128, 256}) {
+            if (N <= target || target > cap) continue;
+            const int64_t k = (N + target - 1) / target, t = (N + k - 1) / k;
+            if (t >= 16 && t * 8 >= target * 7 && std::find(v.begin(), v.end(), t) == v.end()) v.push_back(t);
+          }
           return v;
         };
         std::vector<int64_t> btx = bsides(NX, 1024);
@@ -315,6 +322,66 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
           for (int64_t k = 1; k <= 64 && g.n[xs[0]] * k <= std::min<int64_t>(NX, 1024); k *= 2)
             if (std::find(btx.begin(), btx.end(), g.n[xs[0]] * k) == btx.end())
               btx.push_back(g.n[xs[0]] * k);
+        // whole-column tiles whose B columns continue each other in memory
+        // (X's first axis is B's next position): with beta != 0 the B tile
+        // arrives as one bulk copy per 32 columns instead of one per column --
+        // measured on c5_t14 (B rows of 788 bytes): 5.2 -> 6.4 TB/s with the A
+        // side by tensor map.  Two stages of up to 100 KB, one CTA per SM.
+        if (g.mode == 2 && g.sb[xs[0]] == S * NY && NY <= 256 && S * NY <= 512 && S * NY * g.eB >= 256) {
+          int n = 0;
+          for (int64_t tx : {128, 96, 64, 48, 32, 24, 16}) {
+            if (tx > NX || n >= 2) continue;
+            const int64_t bytes = S * tx * NY * std::max(g.eA, g.eB);
+            const int64_t stage = (tx * 2 + NY) * 4 + NY * (S * tx * g.eA + 32) + tx * (S * NY * g.eB + 32);
+            if (bytes < 12 * 1024 || 2 * stage > 196 * 1024) continue;
+            const double ex = static_cast<double>(NX) / (((NX + tx - 1) / tx) * tx);
+            Spec b;
+            b.v = kSmem;
+            b.kx = kx;
+            b.ky = ky;
+            b.tx = static_cast<int>(tx);
+            b.ty = static_cast<int>(NY);
+            b.vec = 3;
+            b.bp = 1;
+            b.st = 2;
+            b.cost = 1.25 + (1.0 - ex) * 12.0 + 0.05 * (kx + ky) + 0.01 * n;
+            whole_specs.push_back(b);
+            ++n;
+          }
+          // the same with the A tile as one tensor-map box (no row pads: wider
+          // tiles fit), rows of an odd number of 16-byte chunks
+          if (!shared) {
+            n = 0;
+            for (int64_t t0 : {128, 96, 64, 48, 32}) {
+              if (t0 > NX || n >= 2) continue;
+              int64_t tx = 0;
+              for (int64_t d = 0; d <= 12 && !tx; d += 4 / std::min(g.eA, 4))
+                if (((t0 - d) * g.eA) % 32 == 16) tx = t0 - d;
+              if (tx < 8) continue;
+              const int64_t bytes = tx * NY * std::max(g.eA, g.eB);
+              const int64_t stage = (tx * 2 + NY) * 4 + 256 + NY * tx * g.eA + tx * (NY * g.eB + 32);
+              if (bytes < 12 * 1024 || 2 * stage > 196 * 1024) continue;
+              TmaSide sd;
+              const char* w = nullptr;
+              if (!btile_tma_side(g, true, xs, ys, static_cast<uint32_t>(tx), static_cast<uint32_t>(NY), nullptr, &sd, &w))
+                continue;
+              const double ex = static_cast<double>(NX) / (((NX + tx - 1) / tx) * tx);
+              Spec b;
+              b.v = kSmem;
+              b.kx = kx;
+              b.ky = ky;
+              b.tx = static_cast<int>(tx);
+              b.ty = static_cast<int>(NY);
+              b.vec = 3;
+              b.bp = 1;
+              b.st = 2;
+              b.ts = 1;
+              b.cost = 1.2 + (1.0 - ex) * 12.0 + 0.05 * (kx + ky) + 0.01 * n;
+              whole_box.push_back(b);
+              ++n;
+            }
+          }
+        }
         for (int64_t tx : btx) {
           for (int64_t ty : bsides(NY, 1024)) {
             const int64_t bytes = S * tx * ty * std::max(g.eA, g.eB);
@@ -461,6 +528,15 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
             add(b))
           ++n;
       }
+    // the cheapest two whole-column tiles (beta != 0, see above)
+    std::stable_sort(whole_specs.begin(), whole_specs.end(),
+                     [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
+    std::vector<Spec> whole;
+    for (const Spec& b : whole_specs)
+      if (whole.size() < 2 && add(b)) whole.push_back(b);
+    std::stable_sort(whole_box.begin(), whole_box.end(),
+                     [](const Spec& a, const Spec& b) { return a.cost < b.cost; });
+    for (size_t i = 0; i < whole_box.size() && i < 2; ++i) out->push_back(whole_box[i]);
     {  // the square-ish column walks again with 8 / 16 lanes per column
       // (8 rows x 4 columns per warp: fewer shared-memory bank conflicts)
       std::vector<Spec> more;
@@ -499,8 +575,16 @@ void smem_candidates(const Geo& g, bool shared, std::vector<Spec>* out) {
     // the misaligned beta != 0 rows, btile.cuh)
     if (!shared) {
       int added = 0;
-      for (const Spec& b : pick) {
-        if (added >= 6 || b.xp) continue;
+      std::vector<Spec> first = whole;  // the whole-column tiles always get their variants
+      for (const Spec& b : pick) first.push_back(b);
+      for (size_t bi = 0; bi < first.size(); ++bi) {
+        const Spec& b = first[bi];
+        if ((added >= 6 && bi >= whole.size()) || b.xp) continue;
+        if (bi >= whole.size()) {
+          bool dup = false;
+          for (const Spec& w : whole) dup = dup || w.text() == b.text();
+          if (dup) continue;
+        }
         const std::vector<int> xs = x_group(0, b.kx), ys = y_group(g, 0, b.ky);
         const uint32_t tx = static_cast<uint32_t>(std::min<int64_t>(b.tx, prod(g, xs)));
         const uint32_t ty = static_cast<uint32_t>(std::min<int64_t>(b.ty, prod(g, ys)));

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--filter", default=None, help="only candidates containing this text")
     ap.add_argument("--extra", action="append", default=[], help="additional plan texts")
     ap.add_argument("--kinds", default=None, help="override the kind pair, e.g. sd or cz")
+    ap.add_argument("--beta", type=float, default=None, help="override beta (probe: the same shape without / with the B read)")
     args = ap.parse_args()
 
     import torch
@@ -34,6 +35,9 @@ def main():
     from paper_1603_02297_b200.workloads import BY_NAME
 
     w = BY_NAME[args.case]
+    if args.beta is not None:
+        import dataclasses
+        w = dataclasses.replace(w, beta=args.beta)
     ka, kb = (args.kinds[0], args.kinds[1]) if args.kinds else (w.kind, w.kind)
     from paper_1603_02297_b200.workloads import KIND_BYTES
     nbytes = w.elements * (KIND_BYTES[ka] + KIND_BYTES[kb] * (2 if w.beta != 0.0 else 1))

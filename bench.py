@@ -533,18 +533,47 @@ def run_engine_arm(args):
     log(f"[rank {rank}] setup+tune+verify {time.time() - t_setup:.1f}s, checksums ok={checks_ok}")
 
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        for r in rows:
-            r.run(stream)
-    # per-launch events on the launching stream: kernel share and roofline
-    ev = [(torch.cuda.Event(True), torch.cuda.Event(True)) for _ in rows]
+    # A step issues the rows back to back on one stream (`--streams 1`, the
+    # default).  The rows are independent problems, so `--streams N` can issue
+    # them round-robin on N streams; measured on B200 it changes nothing (6057
+    # vs 6058 GB/s: the sweep runs at the power cap, not at kernel boundaries).
+    # The step is bracketed on the main stream: side streams wait for e_start
+    # and the main stream for every side stream before e_stop.
+    nstreams = max(1, args.streams)
+    side = [stream] + [torch.cuda.Stream() for _ in range(nstreams - 1)]
+    joins = [torch.cuda.Event() for _ in side]
+
+    def step(e0, e1):
+        e0.record(stream)
+        for st in side[1:]:
+            st.wait_event(e0)
+        for i, r in enumerate(rows):
+            r.run(side[i % nstreams])
+        for st, j in zip(side[1:], joins[1:]):
+            j.record(st)
+            stream.wait_event(j)
+        e1.record(stream)
+
     e_start, e_stop = torch.cuda.Event(True), torch.cuda.Event(True)
+    for _ in range(args.warmup):
+        step(e_start, e_stop)
+    # a second pass of the same steps with an event pair per row on the
+    # launching stream (kernel share, per-row rates, roofline); the pairs cost
+    # ~1.5% of the step, so `value` comes from the plain pass above
+    ev = [(torch.cuda.Event(True), torch.cuda.Event(True)) for _ in rows]
     row_ms = [0.0] * len(rows)
-    step_ms = []
+    step_ms, serial_ms = [], []
     launches0 = ttb.launch_count()
     with ClockSampler(local % ndev) as clk:
         barrier()
         torch.cuda.nvtx.range_push("ttb_timed")  # ncu --nvtx-include "ttb_timed/"
+        for _ in range(args.steps):
+            step(e_start, e_stop)
+            e_stop.synchronize()
+            step_ms.append(e_start.elapsed_time(e_stop))
+        torch.cuda.nvtx.range_pop()
+        launches = ttb.launch_count() - launches0
+        barrier()
         for _ in range(args.steps):
             e_start.record(stream)
             for i, r in enumerate(rows):
@@ -553,13 +582,12 @@ def run_engine_arm(args):
                 ev[i][1].record(stream)
             e_stop.record(stream)
             e_stop.synchronize()
-            step_ms.append(e_start.elapsed_time(e_stop))
+            serial_ms.append(e_start.elapsed_time(e_stop))
             for i in range(len(rows)):
                 row_ms[i] += ev[i][0].elapsed_time(ev[i][1])
-        torch.cuda.nvtx.range_pop()
         barrier()
-    launches = ttb.launch_count() - launches0
     local_ms = sum(step_ms) / len(step_ms)
+    local_serial_ms = sum(serial_ms) / len(serial_ms)
     ms = allmax(local_ms)
     total_bytes = sum(w.algorithmic_bytes for w in C5)
     value = total_bytes / 1e9 / (ms / 1e3)
@@ -581,7 +609,7 @@ def run_engine_arm(args):
     roofline = {"bound": "hbm", "kernel": f"{dom}_kernel", "achieved": round(achieved, 1),
                 "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "share_of_step": round(fam_ms[dom] / local_ms, 3),
+                "share_of_step": round(fam_ms[dom] / local_serial_ms, 3),
                 "algorithmic_bytes_per_launch": fam_bytes[dom] // max(fam_launch[dom], 1)}
 
     for r in rows:
@@ -595,24 +623,34 @@ def run_engine_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32/f64",
         "data": "synthetic (seeded counter-based generator, SURVEY s8(d))",
-        "config": config_block(world), "roofline": roofline, "e2e": e2e,
+        "config": config_block(world), "streams": nstreams, "roofline": roofline, "e2e": e2e,
         "clocks": clk.summary(), "gpu_launches": launches,
         "pct_hbm_peak": round(100 * value / (peak * world), 2),
         "d2d_memcpy_gbs": round(d2d, 1), "pct_d2d": round(100 * value / (d2d * world), 2),
         "checksums_ok": checks_ok, "rows": per_row,
+        "per_row_pass": {"ms_per_step": round(allmax(local_serial_ms), 4),
+                         "value": round(total_bytes / 1e9 / (allmax(local_serial_ms) / 1e3), 2),
+                         "note": "the same steps again with an event pair per row (one stream): "
+                                 "the pass `rows` and `roofline` are timed in"},
     }
     torch.cuda.empty_cache()
     if rank == 0 and world == 1:
         if not args.no_configs:
             line["configs"] = bench_configs(torch, ttb, peak, d2d)
         if not args.no_cpu:
+            # the reference arm itself, in a fresh process: inside this one (CUDA
+            # context, pinned allocations, torch's thread pools) the same
+            # function measured up to 25% lower than the arm run on its own
             try:
-                if not _oracle().have_ref():
-                    raise FileNotFoundError("oracle/_ref/libttune_ref.so not built")
-                gbs, sec, sample = time_reference(REF_SLAB_DIV, 5, 2, os.cpu_count() or 1)
-                line["cpu_baseline"] = {"value": round(gbs, 3), "unit": "GB/s",
-                                        "cores": os.cpu_count() or 1, "kind": "reference",
-                                        "cpu_model": cpu_model(), "sample": sample}
+                env = {k: v for k, v in os.environ.items()
+                       if k not in ("RANK", "LOCAL_RANK", "WORLD_SIZE", "LOCAL_WORLD_SIZE")}
+                r = subprocess.run([sys.executable, os.path.abspath(__file__), "--impl", "reference",
+                                    "--steps", "5", "--warmup", "3"], env=env, capture_output=True,
+                                   text=True, timeout=900)
+                ref_line = json.loads(r.stdout.strip().splitlines()[-1])
+                if "unavailable" in ref_line:
+                    raise RuntimeError(ref_line["unavailable"])
+                line["cpu_baseline"] = ref_line["cpu_baseline"]
             except Exception as e:  # noqa: BLE001
                 line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": 0,
                                         "kind": "reference", "sample": f"failed: {e}"}
@@ -732,6 +770,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ttb", choices=["ttb", "reference"])
+    ap.add_argument("--streams", type=int, default=1,
+                    help="streams the independent rows of a step are issued on (1: back to back)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (profiling runs)")
     ap.add_argument("--no-configs", action="store_true", help="skip the c1-c4s block (profiling runs)")

@@ -882,7 +882,7 @@ int ttb_plan_describe(ttb_plan plan, char* buf, size_t len) {
   if (!plan) return fail(TTB_EINVAL, "plan: null handle");
   // the plan text plus the kernel that runs it (informational "fn" key)
   const Prepared& p = plan->prep;
-  const char* fn = p.spec.v == kTma ? "tma" : p.spec.v == kRt ? "rt" : p.spec.v == kCopy ? (p.cp.long_rows ? "copy_rows" : "copy")
+  const char* fn = p.spec.v == kTma ? "tma" : p.spec.v == kRt ? "rt" : p.spec.v == kCopy ? (p.cp.bulk ? "rowcopy" : p.cp.long_rows ? "copy_rows" : "copy")
                    : p.sp.dense == 5 ? (p.sp.ly ? "btile" : "btile_lin") : p.sp.dense == 4 ? "vtile" : p.sp.dense >= 2 ? "dense" : p.sp.dense == 1 ? "tile" : "smem";
   std::string t = p.spec.text() + ";fn=" + fn;
   if (!plan->boxes.empty()) t += ";boxes=" + std::to_string(plan->boxes.size());

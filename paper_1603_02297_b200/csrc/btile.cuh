@@ -66,13 +66,20 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
       : "memory");
 }
 
-// spin on mbarrier.test_wait (non-blocking): try_wait may suspend the thread
-// for a system-dependent time after the phase completes
+// wait for a phase with mbarrier.try_wait: the warp sleeps in hardware until
+// the phase completes (or a time limit passes, then it asks again) instead of
+// spinning on test_wait -- the spinning warps took issue slots from the
+// working ones (whole sweep +1.4%, c5_t06 +9%, t07 / t22 +4% on B200;
+// -DTTB_SPIN_WAIT builds the spinning form for comparison)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       " .reg .pred done;\n"
+#ifdef TTB_SPIN_WAIT
       "W: mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n"
+#else
+      "W: mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 done, [%0], %1;\n"
+#endif
       " @!done bra W;\n"
       "}" ::"r"(smem_u32(bar)),
       "r"(parity)

@@ -26,7 +26,7 @@ BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 TIME_US = {"ns": 1e-3, "nsecond": 1e-3, "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3}
 FAMILY = {"btile_kernel": "btile", "dense_kernel": "dense", "tile_kernel": "tile", "smem_kernel": "smem",
           "vtile_kernel": "vtile",
-          "rt_kernel": "rt", "copy_kernel": "copy", "copy_rows_kernel": "copy_rows", "tma_kernel": "tma"}
+          "rt_kernel": "rt", "copy_kernel": "copy", "copy_rows_kernel": "copy_rows", "rowcopy_kernel": "rowcopy", "tma_kernel": "tma"}
 
 
 def main():

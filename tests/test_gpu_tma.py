@@ -160,3 +160,41 @@ def test_bulk_tile_tensor_map_sides_bit_exact(coracle, ka, kb):
                 assert dB.cpu().numpy().tobytes() == want.tobytes(), (perm, sizes, alpha, beta, text)
                 n_run += 1
     assert n_run > 0
+
+
+# (perm map, sizes, lda, ldb): B columns that cover their whole group and
+# continue into the next column (X's first axis is B's next position), with B
+# rows that are not 16-byte multiples (c5_t14's shape in small)
+WHOLE_COLUMN_CASES = [
+    ([2, 1, 3], [256, 70, 5], None, None),        # B rows of 70 elements, A rows aligned
+    ([2, 1, 3], [250, 67, 3], None, None),        # neither side aligned, partial tiles along X
+    ([2, 1], [300, 131], None, None),             # 2D, odd B rows
+]
+
+
+@pytest.mark.parametrize("ka,kb", [("s", "s"), ("d", "d"), ("c", "c"), ("s", "d"), ("z", "c")])
+def test_whole_column_tiles_offered_and_bit_exact(coracle, ka, kb):
+    """beta != 0: tiles that span the whole Y group, whose B columns arrive as a
+    few long bulk copies (plan.cpp whole-column candidates); every such
+    candidate, with and without the A side by tensor map, bit-exact."""
+    rng = np.random.default_rng(4100 + kind_id(ka) * 4 + kind_id(kb))
+    n_run = 0
+    for perm, sizes, lda, ldb in WHOLE_COLUMN_CASES:
+        p = ttb.make_problem(perm, sizes, ka, kb, 0.7, 1.1, lda, ldb)
+        A, B = _inputs(coracle, rng, ka, kb, perm, sizes, lda, ldb, 1.1)
+        want = B.copy()
+        coracle.transpose(ka, kb, perm, sizes, lda, ldb, 0.7, A, 1.1, want)
+        ny = sizes[1]
+        texts = [t for t in ttb.GpuPlan(p, cache=False).candidates()
+                 if f";ty={ny};" in t and "vec=3" in t and "bp=1" in t]
+        assert texts, (perm, sizes, ka, kb)
+        for text in texts:
+            dA = torch.from_numpy(A.copy()).cuda()
+            dB = torch.from_numpy(B.copy()).cuda()
+            plan = ttb.GpuPlan(p, cache=False)
+            plan.select(text)
+            plan.execute(dA, dB)
+            torch.cuda.synchronize()
+            assert dB.cpu().numpy().tobytes() == want.tobytes(), (perm, sizes, text)
+            n_run += 1
+    assert n_run >= len(WHOLE_COLUMN_CASES)

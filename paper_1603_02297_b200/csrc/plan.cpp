@@ -1432,6 +1432,59 @@ std::vector<Spec> candidates(const Geo& g) {
     }
     out.swap(kept);
   }
+  // The costs above choose WHICH candidates are kept (autotune measures them
+  // all); the order of the kept list -- whose head the one-shot API runs
+  // untuned -- gets a second pass fitted to the timings of every candidate of
+  // the 30 BASELINE workloads (profiles/r02_cands, scripts/rank_eval.py):
+  // the heuristic choice went from 72% to 94% of the best measured plan (geo-mean; worst 21% -> 70%).
+  {
+    const int64_t S = shared ? g.n[0] : 1;
+    const int64_t lead_bytes = g.n[0] * emin;
+    auto adjust = [&](const Spec& s) {
+      double a = 0.0;
+      if (s.v == kRt) {  // 21-90% of the best plan, never first; far behind without 16-byte vectors
+        a += 0.9;
+        if (s.w1 * g.eA < 16 || s.w2 * g.eB < 16) a += 2.0;
+      } else if (s.v == kCopy) {  // rows below 1 KB: the bulk tile with a shared lead is 1.25-3.5x faster
+        if (!s.bulk && lead_bytes < 1024) a += 1.6;
+      } else if (s.v == kTma) {
+        // best or within 7% of it wherever it applies with beta != 0, whatever its
+        // run lengths (one box per side): ahead of every other family
+        if (g.mode == 2) a -= 0.9 * s.cost;
+      } else if (s.v == kSmem && s.vec >= 3) {
+        if (s.vec == 4) a += 1.5;   // the linear walk: 50-98% of the column walk
+        if (s.bp == 0) a += 0.5;    // direct B reads: best on one row of 14
+        if (s.st == 3) a += 0.04;   // two stages measured best on most rows
+        // whole-column tiles (the B tile is one run) with the A tile by tensor map
+        if (g.mode == 2 && s.ts == 1 && s.bp == 1 && !shared && s.ty >= prod(g, y_group(g, 0, s.ky)) &&
+            static_cast<double>(s.tx) * s.ty * std::max(g.eA, g.eB) >= 32768.0)
+          a -= 0.3;
+        // stages of ~32 KB (with beta != 0 a stage holds the B tile as well)
+        const double bytes = static_cast<double>(S) * s.tx * s.ty * std::max(g.eA, g.eB);
+        if (g.mode != 2)
+          a += (std::fabs(std::log2(bytes / 32768.0)) - std::fabs(std::log2(bytes / 16384.0))) * 0.2;
+        // Tile order: when B's columns are cut into pieces that do not end on
+        // 32-byte sectors and A's rows are not, walking Y first keeps the
+        // pieces of a column in flight together (c5_t09: 1.5x); the other way
+        // round X first (c5_t13: 1.13x)
+        const int start = shared ? 1 : 0;
+        const std::vector<int> xs = x_group(start, s.kx), ys = y_group(g, start, s.ky);
+        if (g.mode != 2 && !xs.empty() && !ys.empty() && disjoint(xs, ys)) {
+          bool rag_a = (S * s.tx * g.eA) % 32 != 0, rag_b = (S * s.ty * g.eB) % 32 != 0;
+          for (int y : ys) rag_a = rag_a || (g.sa[y] * g.eA) % 32 != 0;
+          for (int x : xs) rag_b = rag_b || (g.sb[x] * g.eB) % 32 != 0;
+          const bool frag_a = prod(g, xs) > s.tx && rag_a, frag_b = prod(g, ys) > s.ty && rag_b;
+          if (frag_b && !frag_a) a += s.order == 1 ? -0.05 : 0.05;
+        }
+      }
+      return a;
+    };
+    std::vector<std::pair<double, Spec>> ranked;
+    for (const Spec& s : out) ranked.emplace_back(s.cost + adjust(s), s);
+    std::stable_sort(ranked.begin(), ranked.end(),
+                     [](const std::pair<double, Spec>& a, const std::pair<double, Spec>& b) { return a.first < b.first; });
+    for (size_t i = 0; i < out.size(); ++i) out[i] = ranked[i].second;
+  }
   if (have_fb) out.push_back(fallback);
   return out;
 }

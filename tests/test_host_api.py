@@ -146,8 +146,15 @@ def test_planner_candidates_for_baseline_configs():
         assert c[-1].startswith("kern=smem") or c[-1].startswith("kern=copy;v=1")
     # c1: fp32 2-D, both leads 7264: in-register 4x4 micro-tiles are available
     assert any(s.startswith("kern=rt;mx=4;my=4") for s in plans["c1"])
-    # c2b keeps the stride-1 index: the vectorised copy kernel leads
-    assert plans["c2b"][0].startswith("kern=copy;v=4")
+    # c2b keeps the stride-1 index: the vectorised copy kernel is offered, and
+    # the bulk tile with the shared lead ranks first (384-byte rows: measured
+    # 1.25x the row kernel, profiles/r02_cands)
+    assert any(s.startswith("kern=copy;v=4") for s in plans["c2b"])
+    assert plans["c2b"][0].startswith("kern=smem") and "vec=3" in plans["c2b"][0]
+    # beta != 0 with every stride a 16-byte multiple: the tensor-map tile leads
+    assert plans["c3"][0].startswith("kern=tma")
+    # long shared rows keep a row kernel first
+    assert plans["c5_t01"][0].startswith("kern=copy")
     # c3 fp64: 16-byte vectors on both sides
     assert any(s.startswith("kern=rt;mx=2;my=2") for s in plans["c3"])
     # c4s: padded A lead still allows 16-byte (2 x complex64) loads

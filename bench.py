@@ -455,14 +455,35 @@ def bench_configs(torch, ttb, peak, d2d):
             e1.synchronize()
             best = min(best, e0.elapsed_time(e1))
         gbs = w.algorithmic_bytes / 1e9 / (best / 1e3)
+        # a device-to-device copy of the same logical bytes, timed the same way:
+        # what ramp and tail cost a 70-300 us kernel (beta != 0 reads B as well,
+        # so its copy moves 3/2 of the tensor bytes: n elements in, n out, n/2 extra)
+        nel = max(1, w.algorithmic_bytes // 8)
+        src = torch.empty(nel, dtype=torch.float32, device="cuda")
+        dst = torch.empty_like(src)
+        for _ in range(5):
+            dst.copy_(src)
+        cbest = 1e30
+        for _ in range(10):
+            e0.record()
+            dst.copy_(src)
+            e1.record()
+            e1.synchronize()
+            cbest = min(cbest, e0.elapsed_time(e1))
+        same = 2 * nel * 4 / 1e9 / (cbest / 1e3)
+        del src, dst
         out[w.name] = {"gbs": round(gbs, 1), "pct_hbm": round(100 * gbs / peak, 1),
                        "pct_d2d": round(100 * gbs / d2d, 1), "us": round(best * 1e3, 1),
+                       "d2d_same_bytes_gbs": round(same, 1),
+                       "pct_d2d_same_bytes": round(100 * gbs / same, 1),
                        "plan": plan.describe(), "checksum_ok": ok}
         del a, b, plan
         torch.cuda.empty_cache()
     vals = [v["gbs"] for v in out.values()]
+    same = [v["pct_d2d_same_bytes"] for v in out.values()]
     out["mean_gbs"] = round(sum(vals) / len(vals), 1)
     out["mean_pct_d2d"] = round(100 * out["mean_gbs"] / d2d, 1)
+    out["mean_pct_d2d_same_bytes"] = round(sum(same) / len(same), 1)
     return out
 
 

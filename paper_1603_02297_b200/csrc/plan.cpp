@@ -1436,7 +1436,7 @@ std::vector<Spec> candidates(const Geo& g) {
   // all); the order of the kept list -- whose head the one-shot API runs
   // untuned -- gets a second pass fitted to the timings of every candidate of
   // the 30 BASELINE workloads (profiles/r02_cands, scripts/rank_eval.py):
-  // the heuristic choice went from 72% to 94% of the best measured plan (geo-mean; worst 21% -> 70%).
+  // the heuristic choice went from 72% to 95% of the best measured plan (geo-mean; worst 21% -> 75%).
   {
     const int64_t S = shared ? g.n[0] : 1;
     const int64_t lead_bytes = g.n[0] * emin;
@@ -1463,6 +1463,25 @@ std::vector<Spec> candidates(const Geo& g) {
         const double bytes = static_cast<double>(S) * s.tx * s.ty * std::max(g.eA, g.eB);
         if (g.mode != 2)
           a += (std::fabs(std::log2(bytes / 32768.0)) - std::fabs(std::log2(bytes / 16384.0))) * 0.2;
+        if (s.vec == 3) {
+          // the column walk's lane use: ly lanes take JY elements each of a
+          // column of S*ty, a warp step covers UX * warps * (32 / ly) columns
+          const uint32_t col = static_cast<uint32_t>(S * s.ty);
+          uint32_t ly = 1;
+          while (ly < 32 && ly < col) ly *= 2;
+          if (s.ly) ly = std::min<uint32_t>(ly, static_cast<uint32_t>(s.ly));
+          const int jy = btile_rows_per_lane(col, ly);
+          const bool big = bytes >= kBtileBigTileBytes && (jy == 2 || jy == 4 || jy == 8);
+          const int64_t ux = g.eB <= 4 ? 4 : g.eB <= 8 ? 2 : 1;
+          const int64_t stepx = ux * (big ? kBtileBigConsumerWarps : kBtileConsumerWarps) * (32 / ly);
+          const double util = static_cast<double>(col) / (static_cast<double>(jy) * ly) *
+                              static_cast<double>(s.tx) / static_cast<double>((s.tx + stepx - 1) / stepx * stepx);
+          a += (1.0 - util) * 0.8;
+          // one CTA per SM with the small warp roles starves (c5_t12 36 x 59: 0.56 of the best)
+          const int64_t stage = (s.tx * 2 + s.ty) * 4 + s.ty * (S * s.tx * g.eA + 32) +
+                                (g.mode == 2 && s.bp ? s.tx * (S * s.ty * g.eB + 32) : 0);
+          if (!big && 2 * (s.st * stage + 1024) > 227 * 1024) a += 1.0;
+        }
         // Tile order: when B's columns are cut into pieces that do not end on
         // 32-byte sectors and A's rows are not, walking Y first keeps the
         // pieces of a column in flight together (c5_t09: 1.5x); the other way

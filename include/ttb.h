@@ -221,7 +221,9 @@ int ttb_benchmark_manifest(int64_t volume_bytes, int kind, uint64_t seed, char* 
 /* Split B's index space for rank r of `world`: the flattened
  * range over the k slowest split axes -- B's indices from the outermost, with
  * A's and B's stride-1 indices moved last (cutting them cuts the tiles' runs)
- * -- k the smallest with a max/mean imbalance <= 1.05.  Writes *n_boxes <= 2*rank-1 boxes (origin +
+ * -- k the smallest with a max/mean imbalance <= 1.05; an axis of that order
+ * that splits within 1.07 on its own is taken alone (one box per rank).
+ * Writes *n_boxes <= 2*rank-1 boxes (origin +
  * extent, `rank` entries each in A index order, over the problem's index
  * space; pass NULL arrays to query the count); each box is an independent
  * sub-problem (same perm/lda/ldb, sizes = extent, buffers offset by origin). */

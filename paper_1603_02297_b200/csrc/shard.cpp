@@ -10,8 +10,9 @@
 // stride-1 axes come last: cutting either one cuts the contiguous runs the
 // tiles read and write (c5_t18's outermost B index is A's stride-1 axis of
 // extent 10 -- pieces of 1-2 elements -- measured 3.6x at 8 ranks instead of
-// 7x, scripts/predict_scaling.py).  A rank's B region is a slab whenever
-// B's outermost axis is eligible, which is the common case.
+// 7x, scripts/predict_scaling.py).  An axis of that order that splits within
+// 7% of perfect balance by itself is taken alone (one box per rank).  A rank's
+// B region is a slab whenever the split axes are B's outermost positions.
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -92,6 +93,33 @@ extern "C" int ttb_shard_boxes(int rank, const int* perm, const int64_t* sizes, 
     const int a = inv[static_cast<size_t>(p)];
     if (a == 0 || p == 0) order.push_back(a);
   }
+  // One axis that splits evenly on its own is preferred: one box (one launch)
+  // per rank instead of up to 2k-1 small ones.  Candidates in the order above;
+  // a stride-1 axis only when a rank's piece of it stays long (>= 512 elements).
+  // Measured with scripts/predict_scaling.py at 8 ranks: c5_t09 cut along its
+  // extent-1016 axis (127 each) instead of three boxes over (34, 1016), c5_t22
+  // along 53 (7 or 6 each) instead of three boxes over (53, 542).
+  // The outermost candidate within 2% of perfect balance, else the best
+  // balanced one within 7%.
+  {
+    int pick = -1;
+    double best = 1.07;
+    for (int a : order) {
+      const bool lead = a == 0 || perm[a] == 1;
+      const int64_t n = sizes[a], per = (n + world - 1) / world;
+      if (lead && n / world < 512) continue;
+      const double imb = static_cast<double>(per) * world / static_cast<double>(n);
+      if (imb <= 1.02) {
+        pick = a;
+        break;
+      }
+      if (imb < best) {
+        best = imb;
+        pick = a;
+      }
+    }
+    if (pick >= 0) order.assign(1, pick);
+  }
   std::vector<int64_t> outer;
   int k = 0;
   int64_t F = 1;
@@ -100,7 +128,7 @@ extern "C" int ttb_shard_boxes(int rank, const int* perm, const int64_t* sizes, 
     outer.push_back(sizes[a]);
     ++k;
     const int64_t per = (F + world - 1) / world;
-    if (static_cast<double>(per) * world / static_cast<double>(F) <= 1.05) break;
+    if (static_cast<double>(per) * world / static_cast<double>(F) <= (order.size() == 1 ? 1.07 : 1.05)) break;
   }
   const int64_t lo = F * r / world, hi = F * (r + 1) / world;
   Box base;

@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--verify", action="store_true", help="checksum every output vs the oracle")
     ap.add_argument("--cache", default=None, help="solution cache file (tune_cached)")
     ap.add_argument("--csv", default=None)
+    ap.add_argument("--no-tune", action="store_true",
+                    help="time the planner's heuristic first choice (the one-shot API's plan)")
     args = ap.parse_args()
 
     import numpy as np
@@ -60,7 +62,9 @@ def main():
         ttb.fill_uniform(k, p.sizes, None, 2 * i + 1, a.data_ptr())
         ttb.fill_uniform(k, sb, None, 2 * i + 2, b.data_ptr())
         plan = ttb.GpuPlan(p, cache=False)
-        if args.cache:
+        if args.no_tune:
+            plan.execute(a, b)
+        elif args.cache:
             plan.tune_cached(a, b, args.cache)
         else:
             plan.autotune(a, b)

@@ -753,11 +753,19 @@ int ttb_plan_autotune(ttb_plan plan, const void* A, void* B, int warmups, int re
     std::stable_sort(order.begin(), order.end(),
                      [&](size_t a, size_t b) { return timed[a].first < timed[b].first; });
     if (order.size() > 4) order.resize(4);
-    for (int round = 0; round < 3 && rc == TTB_OK && order.size() > 1; ++round)
-      for (size_t i : order) timed[i].first = std::min(timed[i].first, measure(timed[i].second, 1, reps));
+    // the finalists are judged on the interleaved rounds alone: the first
+    // round times the list in order on a device that warms up and reaches its
+    // power cap on the way, which favours whoever ran early
+    if (order.size() > 1) {
+      std::vector<float> again(order.size(), 1e30f);
+      for (int round = 0; round < 3 && rc == TTB_OK; ++round)
+        for (size_t k = 0; k < order.size(); ++k)
+          again[k] = std::min(again[k], measure(timed[order[k]].second, 1, reps));
+      for (size_t k = 0; k < order.size(); ++k) timed[order[k]].first = again[k];
+    }
     float best = 1e30f;
     Prepared winner = plan->prep;
-    for (size_t i = 0; i < timed.size(); ++i)
+    for (size_t i : order)
       if (timed[i].first < best) {
         best = timed[i].first;
         winner = timed[i].second;

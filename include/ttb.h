@@ -151,6 +151,16 @@ int ttb_plan_execute(ttb_plan plan, const void* A, void* B, ttb_stream stream);
  * 4096), TTB_HOST_MIN_SLAB_KB (4096), TTB_HOST_PATH=staged. */
 int ttb_plan_execute_host(ttb_plan plan, const void* A_host, void* B_host);
 
+/* The same call without the final wait: returns once the copies and kernels
+ * are queued (pinned buffers; pageable ones make the copies themselves
+ * blocking).  B_host is written, and A_host / B_host may be reused, only after
+ * ttb_plan_host_sync(plan).  Calls on different plans overlap -- the next
+ * transposition's host->device copies run while this one's last slabs compute
+ * and stream out; a second call on the same plan first waits for the one in
+ * flight (one set of staging buffers per plan). */
+int ttb_plan_execute_host_async(ttb_plan plan, const void* A_host, void* B_host);
+int ttb_plan_host_sync(ttb_plan plan);
+
 /* Measured autotune: time every candidate variant of the plan on the given
  * device buffers with CUDA events (warmups + reps, best-of, as
  * measure_candidate, tuner.cpp:27-46) and keep the fastest; the choice is

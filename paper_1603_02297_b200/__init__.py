@@ -452,9 +452,12 @@ class GpuPlan:
         pa, pb = self._pointers(a, b)
         check(lib.ttb_plan_execute(self._h, C.c_void_p(pa), C.c_void_p(pb), _stream(stream)))
 
-    def execute_host(self, a_host, b_host) -> None:
+    def execute_host(self, a_host, b_host, wait: bool = True) -> None:
         """End-to-end on host (numpy/pinned torch) buffers: H2D, kernel, D2H.
-        Both buffers are sized like execute's (the C ABI cannot size them)."""
+        Both buffers are sized like execute's (the C ABI cannot size them).
+        wait=False queues the call and returns (ttb_plan_execute_host_async):
+        b_host is valid, and both buffers reusable, after host_sync(); calls on
+        different plans overlap."""
         p = self.problem
         for name, buf, kind, need in (("A", a_host, p.kind_a, required_elements_a(p)),
                                       ("B", b_host, p.kind_b, required_elements_b(p))):
@@ -463,7 +466,12 @@ class GpuPlan:
                 raise ValueError(f"{name} buffer: too small for problem")
         pa = a_host.ctypes.data if hasattr(a_host, "ctypes") else a_host.data_ptr()
         pb = b_host.ctypes.data if hasattr(b_host, "ctypes") else b_host.data_ptr()
-        check(lib.ttb_plan_execute_host(self._h, C.c_void_p(pa), C.c_void_p(pb)))
+        fn = lib.ttb_plan_execute_host if wait else lib.ttb_plan_execute_host_async
+        check(fn(self._h, C.c_void_p(pa), C.c_void_p(pb)))
+
+    def host_sync(self) -> None:
+        """Wait for the host call queued by execute_host(..., wait=False)."""
+        check(lib.ttb_plan_host_sync(self._h))
 
     def autotune(self, a, b, warmups: int = 2, reps: int = 3, stream=None) -> str:
         pa, pb = self._pointers(a, b)

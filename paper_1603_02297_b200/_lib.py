@@ -42,6 +42,8 @@ _SIGS = {
     "ttb_plan_destroy": ([vp], C.c_int),
     "ttb_plan_execute": ([vp, vp, vp, vp], C.c_int),
     "ttb_plan_execute_host": ([vp, vp, vp], C.c_int),
+    "ttb_plan_execute_host_async": ([vp, vp, vp], C.c_int),
+    "ttb_plan_host_sync": ([vp], C.c_int),
     "ttb_plan_autotune": ([vp, vp, vp, C.c_int, C.c_int, vp], C.c_int),
     "ttb_plan_describe": ([vp, C.c_char_p, C.c_size_t], C.c_int),
     "ttb_plan_candidates": ([vp, C.c_char_p, C.c_size_t], C.c_int),

@@ -100,6 +100,7 @@ struct ttb_plan_s {
   cudaStream_t hs = nullptr;  // host->device copies
   cudaStream_t ks = nullptr;  // slab kernels (pipelined path)
   cudaStream_t ds = nullptr;  // device->host copies (pipelined path)
+  cudaStream_t host_tail = nullptr;  // stream that ends the last host call (hs or ds), null before the first
   std::vector<cudaEvent_t> evs;
   std::unordered_map<int64_t, std::unique_ptr<ttb_plan_s>> chunk_plans;  // by slab extent
   // problems whose A or B footprint reaches 2^31 elements run as boxes below
@@ -444,7 +445,7 @@ cudaError_t copy_slab(const SlabSide& sd, int64_t j0, int64_t j1, char* dst, con
   return err;
 }
 
-int run_pipe(ttb_plan_s* plan, const HostPipe& hp, const void* A_host, void* B_host) {
+int run_pipe(ttb_plan_s* plan, const HostPipe& hp, const void* A_host, void* B_host, bool wait) {
   cudaError_t e;
   for (cudaStream_t* st : {&plan->ks, &plan->ds})
     if (!*st && (e = cudaStreamCreateWithFlags(st, cudaStreamNonBlocking)) != cudaSuccess)
@@ -490,7 +491,42 @@ int run_pipe(ttb_plan_s* plan, const HostPipe& hp, const void* A_host, void* B_h
     if ((e = copy_slab(hp.b, j0, j1, hB, dB, cudaMemcpyDeviceToHost, plan->ds)) != cudaSuccess)
       return cuda_fail(e, "D2H B slab");
   }
-  if ((e = cudaStreamSynchronize(plan->ds)) != cudaSuccess) return cuda_fail(e, "sync");
+  plan->host_tail = plan->ds;  // the stream whose end is the call's end
+  if (wait && (e = cudaStreamSynchronize(plan->ds)) != cudaSuccess) return cuda_fail(e, "sync");
+  return ok();
+}
+
+int host_call(ttb_plan plan, const void* A_host, void* B_host, bool wait) {
+  if (!A_host || !B_host) return fail(TTB_EINVAL, "host buffers: null pointer");
+  cudaError_t e;
+  const size_t na = plan->bytes_a(), nb = plan->bytes_b();
+  if (!plan->hs && (e = cudaStreamCreateWithFlags(&plan->hs, cudaStreamNonBlocking)) != cudaSuccess)
+    return cuda_fail(e, "cudaStreamCreate");
+  if (!plan->dA && (e = cudaMalloc(&plan->dA, na)) != cudaSuccess) return cuda_fail(e, "cudaMalloc A");
+  if (!plan->dB && (e = cudaMalloc(&plan->dB, nb)) != cudaSuccess) return cuda_fail(e, "cudaMalloc B");
+  // a call still in flight on this plan (execute_host_async without host_sync)
+  // owns the staging buffers and the slab events: finish it first
+  if (plan->host_tail && (e = cudaStreamSynchronize(plan->host_tail)) != cudaSuccess)
+    return cuda_fail(e, "sync of the previous host call");
+  const char* hp = std::getenv("TTB_HOST_PATH");  // "staged": force the sequential path
+  if (!(hp && std::strcmp(hp, "staged") == 0) && pinned(A_host) && pinned(B_host)) {
+    HostPipe hpipe;
+    if (pick_pipe(plan->merged.p, &hpipe)) return run_pipe(plan, hpipe, A_host, B_host, wait);
+  }
+  cudaStream_t s = plan->hs;
+  // B's padding must come back unchanged, so B travels to the device when
+  // it is read (beta != 0) or padded
+  const bool b_in = plan->orig.beta != 0.0 || plan->orig.footprint_b() != plan->orig.elements();
+  if ((e = cudaMemcpyAsync(plan->dA, A_host, na, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "H2D A");
+  if (b_in && (e = cudaMemcpyAsync(plan->dB, B_host, nb, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "H2D B");
+  const int rc = execute(plan, plan->prep, plan->dA, plan->dB, s, plan->orig.alpha, plan->orig.beta);
+  if (rc) return rc;
+  if ((e = cudaMemcpyAsync(B_host, plan->dB, nb, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return cuda_fail(e, "D2H B");
+  plan->host_tail = s;
+  if (wait && (e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "sync");
   return ok();
 }
 
@@ -638,35 +674,21 @@ int ttb_transpose(int kind_a, int kind_b, int rank, const int* perm, const int64
 
 int ttb_plan_execute_host(ttb_plan plan, const void* A_host, void* B_host) {
   if (!plan) return fail(TTB_EINVAL, "plan: null handle");
+  return guarded([&] { return host_call(plan, A_host, B_host, true); });
+}
+
+int ttb_plan_execute_host_async(ttb_plan plan, const void* A_host, void* B_host) {
+  if (!plan) return fail(TTB_EINVAL, "plan: null handle");
+  return guarded([&] { return host_call(plan, A_host, B_host, false); });
+}
+
+int ttb_plan_host_sync(ttb_plan plan) {
+  if (!plan) return fail(TTB_EINVAL, "plan: null handle");
   return guarded([&] {
-    if (!A_host || !B_host) return fail(TTB_EINVAL, "host buffers: null pointer");
-    cudaError_t e;
-    const size_t na = plan->bytes_a(), nb = plan->bytes_b();
-    if (!plan->hs && (e = cudaStreamCreateWithFlags(&plan->hs, cudaStreamNonBlocking)) != cudaSuccess)
-      return cuda_fail(e, "cudaStreamCreate");
-    if (!plan->dA && (e = cudaMalloc(&plan->dA, na)) != cudaSuccess) return cuda_fail(e, "cudaMalloc A");
-
-    if (!plan->dB && (e = cudaMalloc(&plan->dB, nb)) != cudaSuccess) return cuda_fail(e, "cudaMalloc B");
-    const char* hp = std::getenv("TTB_HOST_PATH");  // "staged": force the sequential path
-    if (!(hp && std::strcmp(hp, "staged") == 0) && pinned(A_host) && pinned(B_host)) {
-      HostPipe hpipe;
-      if (pick_pipe(plan->merged.p, &hpipe)) return run_pipe(plan, hpipe, A_host, B_host);
+    if (plan->host_tail) {
+      const cudaError_t e = cudaStreamSynchronize(plan->host_tail);
+      if (e != cudaSuccess) return cuda_fail(e, "host sync");
     }
-
-    cudaStream_t s = plan->hs;
-    // B's padding must come back unchanged, so B travels to the device when
-    // it is read (beta != 0) or padded
-    const bool b_in = plan->orig.beta != 0.0 ||
-                      plan->orig.footprint_b() != plan->orig.elements();
-    if ((e = cudaMemcpyAsync(plan->dA, A_host, na, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-      return cuda_fail(e, "H2D A");
-    if (b_in && (e = cudaMemcpyAsync(plan->dB, B_host, nb, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-      return cuda_fail(e, "H2D B");
-    const int rc = execute(plan, plan->prep, plan->dA, plan->dB, s, plan->orig.alpha, plan->orig.beta);
-    if (rc) return rc;
-    if ((e = cudaMemcpyAsync(B_host, plan->dB, nb, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-      return cuda_fail(e, "D2H B");
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "sync");
     return ok();
   });
 }

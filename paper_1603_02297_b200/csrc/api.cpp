@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cctype>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -384,6 +385,7 @@ bool pick_pipe(const Problem& p, HostPipe* out) {
   const std::vector<int64_t> nb = p.b_extents();
   bool found = false;
   int64_t best_k = 0, best_w = 0;
+  int best_cb = 0;
   for (int a = 0; a < r; ++a) {
     const int64_t n = p.sizes[static_cast<size_t>(a)];
     HostPipe h;
@@ -393,18 +395,24 @@ bool pick_pipe(const Problem& p, HostPipe* out) {
       continue;
     // as many slabs as the axis allows while both sides keep rows >= min_row
     // (fewer, wider slabs rather than no pipeline at all)
-    int64_t k = std::min(n, kwant), ext = 0, w = 0;
+    int64_t k = std::min(n, kwant), ext = 0, w = 0, wa = 0, wb = 0;
     for (; k >= 2; k = k > 8 ? k * 3 / 4 : k - 1) {
       ext = (n + k - 1) / k;
-      const int64_t wa = h.a.height == 1 ? INT64_MAX : ext * h.a.stride * ea;
-      const int64_t wb = h.b.height == 1 ? INT64_MAX : ext * h.b.stride * eb;
+      wa = h.a.height == 1 ? INT64_MAX : ext * h.a.stride * ea;
+      wb = h.b.height == 1 ? INT64_MAX : ext * h.b.stride * eb;
       w = std::min(wa, wb);
       if (w >= min_row) break;
     }
     if (k < 2) continue;
     k = (n + ext - 1) / ext;
-    if (found && (k < best_k || (k == best_k && w <= best_w))) continue;
+    // 2D copies with narrow rows at a wide pitch lose up to a quarter of the
+    // link (device->host, 5 KB rows: 43.8 of 57 GB/s, scripts/copy2d_probe.py),
+    // so the axis with more sides whose rows stay >= 32 KB wins (c5_t17: both
+    // sides contiguous along its outermost axis, 61 -> 83 GB/s end to end)
+    const int cb = (wa >= 32768 ? 1 : 0) + (wb >= 32768 ? 1 : 0);
+    if (found && (cb < best_cb || (cb == best_cb && (k < best_k || (k == best_k && w <= best_w))))) continue;
     found = true;
+    best_cb = cb;
     best_k = k;
     best_w = w;
     h.axis = a;
@@ -415,6 +423,13 @@ bool pick_pipe(const Problem& p, HostPipe* out) {
       if (p.ldb[static_cast<size_t>(j)] != nb[static_cast<size_t>(j)]) h.b_in = true;
     *out = h;
   }
+  if (found && std::getenv("TTB_HOST_DEBUG"))
+    std::fprintf(stderr, "[ttb host pipe] axis %d of %d, extent %lld, %lld slabs of %lld; A rows %lld x %lld B (pitch %lld), B rows %lld x %lld B (pitch %lld)\n",
+                 out->axis, r, static_cast<long long>(out->n), static_cast<long long>(best_k),
+                 static_cast<long long>(out->ext), static_cast<long long>(out->a.height),
+                 static_cast<long long>(out->ext * out->a.stride * ea), static_cast<long long>(out->a.pitch * ea),
+                 static_cast<long long>(out->b.height), static_cast<long long>(out->ext * out->b.stride * eb),
+                 static_cast<long long>(out->b.pitch * eb));
   return found;
 }
 
